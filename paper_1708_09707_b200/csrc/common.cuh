@@ -1,0 +1,97 @@
+// common.cuh -- error handling, device buffers and small device helpers.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+namespace hmb {
+
+// Status codes of the C ABI (include/hmat_b200.h); thrown internally and mapped
+// at the boundary like the reference's exception kinds.
+enum Status : int {
+  kOk = 0,
+  kEinval = 1,      // std::invalid_argument
+  kErange = 2,      // std::out_of_range
+  kEnomem = 3,      // allocation failure (device or host)
+  kEcuda = 4,       // CUDA runtime error
+  kEnccl = 5,       // NCCL error
+  kEnonfinite = 6,  // non-finite value (cg_solve, solver.cpp:51-54)
+  kElogic = 7,      // std::logic_error / internal invariant
+};
+
+struct Error : std::runtime_error {
+  Status status;
+  Error(Status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+[[noreturn]] inline void raise(Status s, const std::string& m) { throw Error(s, m); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    const Status s = (e == cudaErrorMemoryAllocation) ? kEnomem : kEcuda;
+    raise(s, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" + std::to_string(line) + ")");
+  }
+}
+#define HM_CUDA(x) ::hmb::cuda_check((x), #x, __FILE__, __LINE__)
+#define HM_LAUNCH_CHECK() ::hmb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// Owning device allocation (cudaMallocAsync on the handle's stream).
+template <class T>
+class DevBuf {
+ public:
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept { swap(o); }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      reset();
+      swap(o);
+    }
+    return *this;
+  }
+  ~DevBuf() { reset(); }
+
+  void alloc(size_t count, cudaStream_t s) {
+    reset();
+    stream_ = s;
+    n_ = count;
+    if (count) HM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), count * sizeof(T), s));
+  }
+  void reset() {
+    if (p_) cudaFreeAsync(p_, stream_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  void zero(cudaStream_t s) {
+    if (n_) HM_CUDA(cudaMemsetAsync(p_, 0, n_ * sizeof(T), s));
+  }
+  void fill_bytes(int v, cudaStream_t s) {
+    if (n_) HM_CUDA(cudaMemsetAsync(p_, v, n_ * sizeof(T), s));
+  }
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+  size_t bytes() const { return n_ * sizeof(T); }
+
+ private:
+  void swap(DevBuf& o) {
+    std::swap(p_, o.p_);
+    std::swap(n_, o.n_);
+    std::swap(stream_, o.stream_);
+  }
+  T* p_ = nullptr;
+  size_t n_ = 0;
+  cudaStream_t stream_ = nullptr;
+};
+
+inline unsigned grid_for(long long n, int threads, long long cap = 1ll << 30) {
+  long long g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<unsigned>(g);
+}
+
+}  // namespace hmb

@@ -1,0 +1,749 @@
+// hm_api.cu -- the C ABI (include/hmat_b200.h): host orchestration in C++,
+// exceptions mapped to hm_status at the boundary.
+#include <nccl.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/hmat_b200.h"
+#include "hmatrix.h"
+#include "primitives.h"
+
+namespace hmb {
+void plan_far_field(HMatrix& h, cudaStream_t s);
+}
+
+using namespace hmb;
+
+struct hm_handle {
+  HMatrix h;
+  std::mutex mu;
+  ncclComm_t comm = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+hm_status guarded(F&& f) {
+  try {
+    f();
+    return HM_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return static_cast<hm_status>(e.status);
+  } catch (const std::bad_alloc& e) {
+    g_err = "host allocation failed";
+    return HM_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HM_ELOGIC;
+  } catch (...) {
+    g_err = "unknown exception";
+    return HM_ELOGIC;
+  }
+}
+
+using Clock = std::chrono::steady_clock;
+double ms_since(Clock::time_point t) { return std::chrono::duration<double, std::milli>(Clock::now() - t).count(); }
+
+KernelParams make_kernel(int kind, double beta, int d) {
+  KernelParams kp{kind, d, 0.0};
+  if (kind == kMatern) {
+    // effective_beta + matern_normalization (core.cpp:83-95), glibc pow/tgamma on the host
+    const double b = beta > 0.0 ? beta : 1.0 + 0.5 * d;
+    const double order = b - 0.5 * d;
+    if (std::fabs(order - 1.0) > 1e-12)
+      raise(kEinval, "Matern kernel: only order beta - d/2 = 1 is supported, got beta = " + std::to_string(b) +
+                         " at d = " + std::to_string(d));
+    kp.matern_norm = 1.0 / (std::pow(2.0, b - 1.0) * std::tgamma(b));
+  } else if (kind != kGaussian) {
+    raise(kEinval, "unknown kernel kind");
+  }
+  return kp;
+}
+
+Config to_config(const hm_config* c) {
+  hm_config def;
+  hm_config_default(&def);
+  if (!c) c = &def;
+  // validate (hmatrix.cpp:20-26)
+  if (c->eta < 0.0) raise(kEinval, "HmatrixConfig: eta must be >= 0");
+  if (c->c_leaf < 1) raise(kEinval, "HmatrixConfig: c_leaf must be >= 1");
+  if (c->k < 1) raise(kEinval, "HmatrixConfig: k must be >= 1");
+  if (c->k > 32) raise(kEinval, "HmatrixConfig: k > 32 is not supported on the device");
+  if (c->bs_aca < 0 || c->bs_dense < 0) raise(kEinval, "HmatrixConfig: batch sizes must be >= 0");
+  if (c->has_epsilon && c->epsilon <= 0.0) raise(kEinval, "HmatrixConfig: epsilon must be > 0");
+  if (c->adm_mode < 0 || c->adm_mode > 2) raise(kEinval, "HmatrixConfig: bad admissibility mode");
+  if (c->world < 1 || c->rank < 0 || c->rank >= c->world) raise(kEinval, "HmatrixConfig: bad rank/world");
+  Config cfg;
+  cfg.eta = c->eta;
+  cfg.c_leaf = c->c_leaf;
+  cfg.k = c->k;
+  cfg.bs_aca = c->bs_aca;
+  cfg.bs_dense = c->bs_dense;
+  cfg.precompute_aca = c->precompute_aca != 0;
+  cfg.has_epsilon = c->has_epsilon != 0;
+  cfg.epsilon = c->epsilon;
+  cfg.mode = c->adm_mode;
+  cfg.near_stored = c->near_stored ? 1 : 0;
+  cfg.rank = c->rank;
+  cfg.world = c->world;
+  cfg.aca_chunk_rows = c->aca_chunk_rows;
+  return cfg;
+}
+
+void require_device() {
+  int nd = 0;
+  if (cudaGetDeviceCount(&nd) != cudaSuccess || nd == 0) raise(kEcuda, "no CUDA device available");
+}
+
+void setup_common(hm_handle* H, const double* coords_dev, long long n, int d) {
+  HMatrix& h = H->h;
+  const auto t0 = Clock::now();
+  build_hmatrix(h, coords_dev);
+  // partition_dense_queue throws when one block exceeds a positive bs_dense (dense_blocks.cpp:44-46)
+  if (h.cfg.bs_dense > 0) {
+    for (long long b = 0; b < h.dense.count; ++b)
+      if (static_cast<long long>(h.dense.h_m[b]) * h.dense.h_n[b] > h.cfg.bs_dense)
+        raise(kEinval, "partition_dense_queue: a single block exceeds bs_dense");
+  }
+  h.xm.alloc(n, h.stream);
+  h.zm.alloc(n, h.stream);
+  h.zm.zero(h.stream);
+  const auto ta = Clock::now();
+  plan_far_field(h, h.stream);
+  HM_CUDA(cudaStreamSynchronize(h.stream));
+  h.tm.aca_ms = ms_since(ta);
+  const auto tn = Clock::now();
+  if (h.cfg.near_stored) store_near_field(h, h.stream);
+  HM_CUDA(cudaStreamSynchronize(h.stream));
+  h.tm.near_ms = ms_since(tn);
+  h.tm.setup_ms = ms_since(t0);
+  (void)d;
+}
+
+hm_handle* new_handle(const hm_config* cfg, long long n, int d, int kernel, double beta) {
+  require_device();
+  auto H = std::make_unique<hm_handle>();
+  H->h.cfg = to_config(cfg);
+  H->h.device = cfg ? cfg->device : 0;
+  HM_CUDA(cudaSetDevice(H->h.device));
+  HM_CUDA(cudaStreamCreateWithFlags(&H->h.stream, cudaStreamNonBlocking));
+  H->h.kp = make_kernel(kernel, beta, d);
+  H->h.n = n;
+  H->h.d = d;
+  if (n < 1) raise(kEinval, "build_block_cluster_tree: empty point set");
+  if (d < 1 || d > 20) raise(kEinval, "dimension must be in [1, 20]");
+  return H.release();
+}
+
+// ---------------------------------------------------------------- small kernels
+__global__ void eval_pairs_kernel(KernelParams kp, int d, long long n, const double* y, const double* yp,
+                                  double* out) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double r2 = 0.0;
+    for (int a = 0; a < d; ++a) {
+      const double dx = hsub(y[a * n + i], yp[a * n + i]);
+      r2 = hadd(r2, hmul(dx, dx));
+    }
+    out[i] = phi_r2(kp, r2);
+  }
+}
+
+__global__ void exp_port_kernel(long long n, const double* x, double* out) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    out[i] = glibc_exp(x[i]);
+}
+
+// exact product, one thread per Morton row, acc += phi(i,j) * x_m[j] sequentially
+// (relative_error hmatrix.cpp:136-143 and oracle.cpp:41-49 order)
+__global__ void dense_exact_kernel(const double* __restrict__ coords, long long n, int d, KernelParams kp,
+                                   const double* __restrict__ xm, long long row_begin, long long row_end,
+                                   double* __restrict__ zm) {
+  const long long i = row_begin + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= row_end) return;
+  double yi[20];
+  for (int a = 0; a < d; ++a) yi[a] = coords[a * n + i];
+  double acc = 0.0;
+  for (long long j = 0; j < n; ++j) {
+    double r2 = 0.0;
+    for (int a = 0; a < d; ++a) {
+      const double dx = hsub(yi[a], __ldg(coords + a * n + j));
+      r2 = hadd(r2, hmul(dx, dx));
+    }
+    acc = hadd(acc, hmul(phi_r2(kp, r2), __ldg(xm + j)));
+  }
+  zm[i] = acc;
+}
+
+__global__ void gather_kernel(const double* __restrict__ x, const long long* __restrict__ perm, long long n,
+                              double* __restrict__ xm) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    xm[i] = x[perm[i]];
+}
+__global__ void scatter_kernel(const double* __restrict__ zm, const long long* __restrict__ perm, long long n,
+                               double* __restrict__ z) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    z[perm[i]] = zm[i];
+}
+
+// fixed-order deterministic dot: per-block tree partials, then one block folds them
+__global__ void dot_partial_kernel(const double* a, const double* b, long long n, double* part) {
+  __shared__ double sm[256];
+  double acc = 0.0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    acc = hadd(acc, hmul(a[i], b[i]));
+  sm[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s; s >>= 1) {
+    if (threadIdx.x < s) sm[threadIdx.x] = hadd(sm[threadIdx.x], sm[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sm[0];
+}
+__global__ void dot_final_kernel(const double* part, int nb, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double acc = 0.0;
+    for (int i = 0; i < nb; ++i) acc = hadd(acc, part[i]);
+    *out = acc;
+  }
+}
+
+// CG vector updates (solver.cpp:27-31, 46-49, 59-61)
+__global__ void axpy_sigma_kernel(double* ap, const double* p, double sigma2, long long n) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    ap[i] = hadd(ap[i], hmul(sigma2, p[i]));
+}
+__global__ void cg_update_kernel(double* x, double* r, const double* p, const double* ap, const double* alpha_p,
+                                 long long n) {
+  const double alpha = *alpha_p;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    x[i] = hadd(x[i], hmul(alpha, p[i]));
+    r[i] = hsub(r[i], hmul(alpha, ap[i]));
+  }
+}
+__global__ void cg_dir_kernel(double* p, const double* r, double beta, long long n) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    p[i] = hadd(r[i], hmul(beta, p[i]));
+}
+
+constexpr int kDotBlocks = 1184;  // 8 x 148 SMs
+
+double device_dot(const double* a, const double* b, long long n, DevBuf<double>& part, cudaStream_t s) {
+  if (part.size() < kDotBlocks + 1) part.alloc(kDotBlocks + 1, s);
+  dot_partial_kernel<<<kDotBlocks, 256, 0, s>>>(a, b, n, part.get());
+  dot_final_kernel<<<1, 32, 0, s>>>(part.get(), kDotBlocks, part.get() + kDotBlocks);
+  HM_LAUNCH_CHECK();
+  double out = 0.0;
+  HM_CUDA(cudaMemcpyAsync(&out, part.get() + kDotBlocks, sizeof(double), cudaMemcpyDeviceToHost, s));
+  HM_CUDA(cudaStreamSynchronize(s));
+  return out;
+}
+
+// z (original order, device) = H x, with the row-sliced allgather when world > 1
+void product(hm_handle* H, const double* x_dev, double* z_dev, cudaStream_t s) {
+  HMatrix& h = H->h;
+  const long long n = h.n;
+  gather_kernel<<<grid_for(n, 256, 1 << 16), 256, 0, s>>>(x_dev, h.perm.get(), n, h.xm.get());
+  HM_LAUNCH_CHECK();
+  mvp_morton(h, s);
+  if (h.cfg.world > 1) {
+    if (!H->comm) raise(kEnccl, "world > 1 but no NCCL communicator attached (hm_attach_nccl)");
+    // each rank's Morton row slice is broadcast in place (slices are contiguous, sizes may differ)
+    std::vector<long long> bounds(h.cfg.world + 1);
+    int g = 0;
+    while ((1 << g) < h.cfg.world) ++g;
+    for (int r = 0; r <= h.cfg.world; ++r) {
+      long long v = n;
+      if (r < h.cfg.world)
+        HM_CUDA(cudaMemcpy(&v, h.slot_lo.get() + h.depth_base[g] + r, sizeof(long long), cudaMemcpyDeviceToHost));
+      bounds[r] = v;
+    }
+    if (ncclGroupStart() != ncclSuccess) raise(kEnccl, "ncclGroupStart");
+    for (int r = 0; r < h.cfg.world; ++r) {
+      double* p = h.zm.get() + bounds[r];
+      if (ncclBroadcast(p, p, static_cast<size_t>(bounds[r + 1] - bounds[r]), ncclDouble, r, H->comm, s) !=
+          ncclSuccess)
+        raise(kEnccl, "ncclBroadcast of the y slice failed");
+    }
+    if (ncclGroupEnd() != ncclSuccess) raise(kEnccl, "ncclGroupEnd");
+  }
+  scatter_kernel<<<grid_for(n, 256, 1 << 16), 256, 0, s>>>(h.zm.get(), h.perm.get(), n, z_dev);
+  HM_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hm_last_error(void) { return g_err.c_str(); }
+
+void hm_config_default(hm_config* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->eta = 1.5;
+  c->c_leaf = 256;
+  c->k = 16;
+  c->bs_aca = 1ll << 20;
+  c->bs_dense = 1ll << 22;
+  c->world = 1;
+}
+
+int hm_device_count(void) {
+  int nd = 0;
+  if (cudaGetDeviceCount(&nd) != cudaSuccess) return 0;
+  return nd;
+}
+
+hm_status hm_setup(const double* coords, int64_t n, int32_t d, int32_t kernel, double beta, const hm_config* cfg,
+                   hm_handle** out) {
+  *out = nullptr;
+  hm_handle* H = nullptr;
+  const hm_status st = guarded([&] {
+    if (!coords) raise(kEinval, "coords is null");
+    H = new_handle(cfg, n, d, kernel, beta);
+    DevBuf<double> c;
+    c.alloc(static_cast<size_t>(n) * d, H->h.stream);
+    HM_CUDA(cudaMemcpyAsync(c.get(), coords, sizeof(double) * n * d, cudaMemcpyHostToDevice, H->h.stream));
+    setup_common(H, c.get(), n, d);
+  });
+  if (st != HM_OK) {
+    delete H;
+    return st;
+  }
+  *out = H;
+  return HM_OK;
+}
+
+hm_status hm_setup_device(const double* coords_dev, int64_t n, int32_t d, int32_t kernel, double beta,
+                          const hm_config* cfg, hm_handle** out) {
+  *out = nullptr;
+  hm_handle* H = nullptr;
+  const hm_status st = guarded([&] {
+    if (!coords_dev) raise(kEinval, "coords is null");
+    H = new_handle(cfg, n, d, kernel, beta);
+    setup_common(H, coords_dev, n, d);
+  });
+  if (st != HM_OK) {
+    delete H;
+    return st;
+  }
+  *out = H;
+  return HM_OK;
+}
+
+void hm_destroy(hm_handle* H) {
+  if (!H) return;
+  cudaSetDevice(H->h.device);
+  if (H->comm) ncclCommDestroy(H->comm);
+  cudaStream_t s = H->h.stream;
+  cudaStreamSynchronize(s);
+  delete H;  // buffers are freed on the stream
+  if (s) {
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  }
+}
+
+hm_status hm_mvp(hm_handle* H, const double* x, double* z, hm_timings* t) {
+  return guarded([&] {
+    if (!H || !x || !z) raise(kEinval, "mvp: null argument");
+    std::lock_guard<std::mutex> lock(H->mu);
+    HMatrix& h = H->h;
+    HM_CUDA(cudaSetDevice(h.device));
+    const auto t0 = Clock::now();
+    cudaStream_t s = h.stream;
+    if (h.xin.size() < static_cast<size_t>(h.n)) h.xin.alloc(h.n, s);
+    if (h.zout.size() < static_cast<size_t>(h.n)) h.zout.alloc(h.n, s);
+    HM_CUDA(cudaMemcpyAsync(h.xin.get(), x, sizeof(double) * h.n, cudaMemcpyHostToDevice, s));
+    product(H, h.xin.get(), h.zout.get(), s);
+    HM_CUDA(cudaMemcpyAsync(z, h.zout.get(), sizeof(double) * h.n, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+    h.tm.mvp_ms = ms_since(t0);
+    if (t) hm_get_timings(H, t);
+  });
+}
+
+hm_status hm_mvp_device(hm_handle* H, const double* x_dev, double* z_dev, void* stream) {
+  return guarded([&] {
+    if (!H || !x_dev || !z_dev) raise(kEinval, "mvp: null argument");
+    std::lock_guard<std::mutex> lock(H->mu);
+    HM_CUDA(cudaSetDevice(H->h.device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : H->h.stream;
+    product(H, x_dev, z_dev, s);
+  });
+}
+
+hm_status hm_nccl_unique_id(unsigned char id[128]) {
+  return guarded([&] {
+    ncclUniqueId u;
+    if (ncclGetUniqueId(&u) != ncclSuccess) raise(kEnccl, "ncclGetUniqueId failed");
+    static_assert(sizeof(u) == 128, "ncclUniqueId size");
+    std::memcpy(id, &u, 128);
+  });
+}
+
+hm_status hm_attach_nccl(hm_handle* H, const unsigned char id[128]) {
+  return guarded([&] {
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    HM_CUDA(cudaSetDevice(H->h.device));
+    if (ncclCommInitRank(&H->comm, H->h.cfg.world, u, H->h.cfg.rank) != ncclSuccess)
+      raise(kEnccl, "ncclCommInitRank failed");
+  });
+}
+
+hm_status hm_cg_solve(hm_handle* H, const double* b, double sigma2, double tol, int64_t max_iter, double* x,
+                      int64_t* iterations, double* rel_res) {
+  return guarded([&] {
+    // solver.cpp:19-73
+    std::lock_guard<std::mutex> lock(H->mu);
+    HMatrix& h = H->h;
+    if (tol <= 0.0) raise(kEinval, "cg_solve: tol must be > 0");
+    if (max_iter < 1) raise(kEinval, "cg_solve: max_iter must be >= 1");
+    if (sigma2 < 0.0) raise(kEinval, "cg_solve: sigma2 must be >= 0");
+    HM_CUDA(cudaSetDevice(h.device));
+    cudaStream_t s = h.stream;
+    const long long n = h.n;
+    DevBuf<double> db, dx, dr, dp, dap, part, alpha;
+    db.alloc(n, s);
+    dx.alloc(n, s);
+    dr.alloc(n, s);
+    dp.alloc(n, s);
+    dap.alloc(n, s);
+    alpha.alloc(1, s);
+    HM_CUDA(cudaMemcpyAsync(db.get(), b, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    dx.zero(s);
+    *iterations = 0;
+    *rel_res = 0.0;
+    const double b_norm = std::sqrt(device_dot(db.get(), db.get(), n, part, s));
+    if (b_norm == 0.0) {
+      std::memset(x, 0, sizeof(double) * n);
+      return;
+    }
+    HM_CUDA(cudaMemcpyAsync(dr.get(), db.get(), sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    HM_CUDA(cudaMemcpyAsync(dp.get(), db.get(), sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    double rs = device_dot(dr.get(), dr.get(), n, part, s);
+    const unsigned grid = grid_for(n, 256, 1 << 16);
+    for (long long iter = 1; iter <= max_iter; ++iter) {
+      product(H, dp.get(), dap.get(), s);
+      axpy_sigma_kernel<<<grid, 256, 0, s>>>(dap.get(), dp.get(), sigma2, n);
+      HM_LAUNCH_CHECK();
+      const double a = rs / device_dot(dp.get(), dap.get(), n, part, s);
+      HM_CUDA(cudaMemcpyAsync(alpha.get(), &a, sizeof(double), cudaMemcpyHostToDevice, s));
+      cg_update_kernel<<<grid, 256, 0, s>>>(dx.get(), dr.get(), dp.get(), dap.get(), alpha.get(), n);
+      HM_LAUNCH_CHECK();
+      const double rs_next = device_dot(dr.get(), dr.get(), n, part, s);
+      if (!std::isfinite(rs_next) || !std::isfinite(a))
+        raise(kEnonfinite, "cg_solve: non-finite value at iteration " + std::to_string(iter) + " (residual " +
+                               std::to_string(std::sqrt(std::fabs(rs)) / b_norm) + ")");
+      *iterations = iter;
+      if (std::sqrt(rs_next) <= tol * b_norm) break;
+      const double beta = rs_next / rs;
+      cg_dir_kernel<<<grid, 256, 0, s>>>(dp.get(), dr.get(), beta, n);
+      HM_LAUNCH_CHECK();
+      rs = rs_next;
+    }
+    // true residual of the returned iterate (solver.cpp:64-71)
+    product(H, dx.get(), dap.get(), s);
+    axpy_sigma_kernel<<<grid, 256, 0, s>>>(dap.get(), dx.get(), sigma2, n);
+    HM_LAUNCH_CHECK();
+    std::vector<double> ax(n);
+    HM_CUDA(cudaMemcpyAsync(ax.data(), dap.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaMemcpyAsync(x, dx.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+    double diff_sq = 0.0;
+    for (long long i = 0; i < n; ++i) {
+      const double dd = b[i] - ax[i];
+      diff_sq += dd * dd;
+    }
+    *rel_res = std::sqrt(diff_sq) / b_norm;
+  });
+}
+
+hm_status hm_dense_mvp(hm_handle* H, const double* x, double* z) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lock(H->mu);
+    HMatrix& h = H->h;
+    HM_CUDA(cudaSetDevice(h.device));
+    cudaStream_t s = h.stream;
+    const long long n = h.n;
+    DevBuf<double> dx, dz, dzm;
+    dx.alloc(n, s);
+    dz.alloc(n, s);
+    dzm.alloc(n, s);
+    HM_CUDA(cudaMemcpyAsync(dx.get(), x, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    gather_kernel<<<grid_for(n, 256, 1 << 16), 256, 0, s>>>(dx.get(), h.perm.get(), n, h.xm.get());
+    dense_exact_kernel<<<grid_for(n, 128), 128, 0, s>>>(h.coords.get(), n, h.d, h.kp, h.xm.get(), 0, n, dzm.get());
+    scatter_kernel<<<grid_for(n, 256, 1 << 16), 256, 0, s>>>(dzm.get(), h.perm.get(), n, dz.get());
+    HM_LAUNCH_CHECK();
+    HM_CUDA(cudaMemcpyAsync(z, dz.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+hm_status hm_relative_error(hm_handle* H, const double* x, double* out) {
+  // hmatrix.cpp:125-153 without the N limit (the exact product runs on the device)
+  std::vector<double> zh(H->h.n), ze(H->h.n);
+  hm_status st = hm_mvp(H, x, zh.data(), nullptr);
+  if (st != HM_OK) return st;
+  st = hm_dense_mvp(H, x, ze.data());
+  if (st != HM_OK) return st;
+  double diff_sq = 0.0, ref_sq = 0.0;
+  for (long long i = 0; i < H->h.n; ++i) {
+    const double d = zh[i] - ze[i];
+    diff_sq += d * d;
+    ref_sq += ze[i] * ze[i];
+  }
+  *out = std::sqrt(diff_sq) / std::sqrt(ref_sq);
+  return HM_OK;
+}
+
+hm_status hm_get_timings(hm_handle* H, hm_timings* t) {
+  return guarded([&] {
+    const Timings& tm = H->h.tm;
+    t->setup_ms = tm.setup_ms;
+    t->morton_ms = tm.morton_ms;
+    t->tree_ms = tm.tree_ms;
+    t->aca_ms = tm.aca_ms;
+    t->near_ms = tm.near_ms;
+    t->mvp_ms = tm.mvp_ms;
+  });
+}
+
+hm_status hm_get_stats(hm_handle* H, hm_stats* st) {
+  return guarded([&] {
+    const HMatrix& h = H->h;
+    st->n_dense = h.dense.count;
+    st->n_aca = h.aca.count;
+    st->S_d = h.S_d;
+    st->S_l = h.S_l;
+    st->sum_m_adm = h.sum_m_adm;
+    st->sum_n_adm = h.sum_n_adm;
+    st->aca_rejections = h.aca_rejections;
+    st->dmax_leaf = h.dmax_leaf;
+    st->row_begin = h.row_begin;
+    st->row_end = h.row_end;
+    st->device_bytes = static_cast<double>(h.dense_vals.bytes() + h.U.bytes() + h.V.bytes() + h.coords.bytes());
+  });
+}
+
+hm_status hm_get_points(hm_handle* H, double* coords, int64_t* perm) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lock(H->mu);
+    HMatrix& h = H->h;
+    HM_CUDA(cudaSetDevice(h.device));
+    HM_CUDA(cudaMemcpyAsync(coords, h.coords.get(), sizeof(double) * h.n * h.d, cudaMemcpyDeviceToHost, h.stream));
+    HM_CUDA(cudaMemcpyAsync(perm, h.perm.get(), sizeof(long long) * h.n, cudaMemcpyDeviceToHost, h.stream));
+    HM_CUDA(cudaStreamSynchronize(h.stream));
+  });
+}
+
+hm_status hm_get_codes(hm_handle* H, uint64_t* codes) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lock(H->mu);
+    HMatrix& h = H->h;
+    HM_CUDA(cudaSetDevice(h.device));
+    HM_CUDA(cudaMemcpyAsync(codes, h.codes.get(), sizeof(uint64_t) * h.n, cudaMemcpyDeviceToHost, h.stream));
+    HM_CUDA(cudaStreamSynchronize(h.stream));
+  });
+}
+
+hm_status hm_get_leaves(hm_handle* H, int32_t which, int64_t* rows4, double* boxes) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lock(H->mu);
+    HMatrix& h = H->h;
+    HM_CUDA(cudaSetDevice(h.device));
+    const LeafList& l = which == 0 ? h.dense : h.aca;
+    const long long cnt = l.count;
+    for (long long i = 0; i < cnt; ++i) {
+      rows4[4 * i + 0] = l.h_rl[i];
+      rows4[4 * i + 1] = static_cast<long long>(l.h_rl[i]) + l.h_m[i];
+      rows4[4 * i + 2] = l.h_cl[i];
+      rows4[4 * i + 3] = static_cast<long long>(l.h_cl[i]) + l.h_n[i];
+    }
+    if (boxes && cnt) {
+      const int d = h.d;
+      std::vector<int> ts(cnt), ss(cnt);
+      std::vector<double> tab(static_cast<size_t>(h.nslots) * 2 * d);
+      HM_CUDA(cudaMemcpyAsync(ts.data(), l.tau_slot.get(), sizeof(int) * cnt, cudaMemcpyDeviceToHost, h.stream));
+      HM_CUDA(cudaMemcpyAsync(ss.data(), l.sigma_slot.get(), sizeof(int) * cnt, cudaMemcpyDeviceToHost, h.stream));
+      HM_CUDA(cudaMemcpyAsync(tab.data(), h.boxes.get(), sizeof(double) * tab.size(), cudaMemcpyDeviceToHost,
+                              h.stream));
+      HM_CUDA(cudaStreamSynchronize(h.stream));
+      for (long long i = 0; i < cnt; ++i) {
+        std::memcpy(boxes + 4 * d * i, tab.data() + static_cast<size_t>(ts[i]) * 2 * d, sizeof(double) * 2 * d);
+        std::memcpy(boxes + 4 * d * i + 2 * d, tab.data() + static_cast<size_t>(ss[i]) * 2 * d, sizeof(double) * 2 * d);
+      }
+    }
+  });
+}
+
+hm_status hm_get_aca(hm_handle* H, int64_t* k_eff, int64_t* row_piv, int64_t* col_piv, double* u, double* v) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lock(H->mu);
+    HMatrix& h = H->h;
+    HM_CUDA(cudaSetDevice(h.device));
+    cudaStream_t s = h.stream;
+    const long long cnt = h.aca.count, kmax = h.cfg.k;
+    if (h.cfg.world > 1) raise(kEinval, "hm_get_aca: single-rank handles only");
+    std::vector<long long> uo(cnt + 1, 0), vo(cnt + 1, 0);
+    for (long long b = 0; b < cnt; ++b) {
+      uo[b + 1] = uo[b] + kmax * h.aca.h_m[b];
+      vo[b + 1] = vo[b] + kmax * h.aca.h_n[b];
+    }
+    if (!h.factors_valid) {
+      // recompute mode: factorise everything once into scratch (introspection only)
+      h.U.alloc(std::max(uo[cnt], 1ll), s);
+      h.V.alloc(std::max(vo[cnt], 1ll), s);
+      compute_aca(h, 0, cnt, s);
+    }
+    std::vector<int> hk(cnt), hrp(cnt * kmax), hcp(cnt * kmax);
+    if (cnt) {
+      HM_CUDA(cudaMemcpyAsync(hk.data(), h.k_eff.get(), sizeof(int) * cnt, cudaMemcpyDeviceToHost, s));
+      HM_CUDA(cudaMemcpyAsync(hrp.data(), h.row_piv.get(), sizeof(int) * cnt * kmax, cudaMemcpyDeviceToHost, s));
+      HM_CUDA(cudaMemcpyAsync(hcp.data(), h.col_piv.get(), sizeof(int) * cnt * kmax, cudaMemcpyDeviceToHost, s));
+    }
+    std::vector<double> hu, hv;
+    if (u || v) {
+      hu.resize(uo[cnt]);
+      hv.resize(vo[cnt]);
+      if (cnt) {
+        HM_CUDA(cudaMemcpyAsync(hu.data(), h.U.get(), sizeof(double) * uo[cnt], cudaMemcpyDeviceToHost, s));
+        HM_CUDA(cudaMemcpyAsync(hv.data(), h.V.get(), sizeof(double) * vo[cnt], cudaMemcpyDeviceToHost, s));
+      }
+    }
+    HM_CUDA(cudaStreamSynchronize(s));
+    if (!h.factors_valid) {
+      h.U.reset();
+      h.V.reset();
+    }
+    for (long long b = 0; b < cnt; ++b) {
+      k_eff[b] = hk[b];
+      const long long m = h.aca.h_m[b], n = h.aca.h_n[b];
+      for (long long l = 0; l < kmax; ++l) {
+        row_piv[b * kmax + l] = hrp[b * kmax + l];
+        col_piv[b * kmax + l] = hcp[b * kmax + l];
+        const bool live = l < hk[b];
+        if (u)
+          for (long long i = 0; i < m; ++i) u[uo[b] + l * m + i] = live ? hu[uo[b] + l * m + i] : 0.0;
+        if (v)
+          for (long long j = 0; j < n; ++j) v[vo[b] + l * n + j] = live ? hv[vo[b] + j * kmax + l] : 0.0;
+      }
+    }
+  });
+}
+
+hm_status hm_morton_codes(const double* coords, int64_t n, int32_t d, uint64_t* codes) {
+  return guarded([&] {
+    require_device();
+    if (d < 1 || d > 20) raise(kEinval, "morton_bits_per_dim: dimension out of range");
+    cudaStream_t s = nullptr;
+    DevBuf<double> c;
+    DevBuf<unsigned long long> k;
+    c.alloc(static_cast<size_t>(n) * d, s);
+    k.alloc(n, s);
+    HM_CUDA(cudaMemcpyAsync(c.get(), coords, sizeof(double) * n * d, cudaMemcpyHostToDevice, s));
+    if (n) morton_codes_device(c.get(), n, d, k.get(), s);
+    HM_CUDA(cudaMemcpyAsync(codes, k.get(), sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+hm_status hm_morton_order(const double* coords, int64_t n, int32_t d, const int64_t* perm_in, double* coords_out,
+                          int64_t* perm_out) {
+  return guarded([&] {
+    require_device();
+    if (d < 1 || d > 20) raise(kEinval, "morton_bits_per_dim: dimension out of range");
+    if (n < 1) return;
+    cudaStream_t s = nullptr;
+    DevBuf<double> c, co;
+    DevBuf<unsigned long long> k;
+    DevBuf<unsigned> ord;
+    c.alloc(static_cast<size_t>(n) * d, s);
+    co.alloc(static_cast<size_t>(n) * d, s);
+    k.alloc(n, s);
+    ord.alloc(n, s);
+    HM_CUDA(cudaMemcpyAsync(c.get(), coords, sizeof(double) * n * d, cudaMemcpyHostToDevice, s));
+    morton_codes_device(c.get(), n, d, k.get(), s);
+    iota_u32(ord.get(), n, s);
+    radix_sort_pairs(k.get(), ord.get(), n, s);
+    std::vector<unsigned> ho(n);
+    std::vector<double> hc(static_cast<size_t>(n) * d);
+    HM_CUDA(cudaMemcpyAsync(ho.data(), ord.get(), sizeof(unsigned) * n, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+    for (long long i = 0; i < n; ++i) {
+      const long long src = ho[i];
+      for (int a = 0; a < d; ++a) coords_out[a * n + i] = coords[a * n + src];
+      perm_out[i] = perm_in ? perm_in[src] : src;
+    }
+  });
+}
+
+hm_status hm_aca_dense(int64_t nb, const int64_t* shapes, const double* entries, int64_t kmax, int32_t has_eps,
+                       double eps, double eta, int64_t* k_eff, int64_t* row_piv, int64_t* col_piv, double* u,
+                       double* v) {
+  return guarded([&] {
+    require_device();
+    if (nb <= 0) return;
+    aca_dense_blocks(nb, reinterpret_cast<const long long*>(shapes), entries, kmax, has_eps != 0, eps, eta,
+                     reinterpret_cast<long long*>(k_eff), reinterpret_cast<long long*>(row_piv),
+                     reinterpret_cast<long long*>(col_piv), u, v, nullptr);
+  });
+}
+
+hm_status hm_eval_kernel(int32_t kernel, double beta, int32_t d, int64_t n, const double* y, const double* yp,
+                         double* out) {
+  return guarded([&] {
+    require_device();
+    const KernelParams kp = make_kernel(kernel, beta, d);
+    if (n <= 0) return;
+    cudaStream_t s = nullptr;
+    DevBuf<double> a, b, o;
+    a.alloc(static_cast<size_t>(n) * d, s);
+    b.alloc(static_cast<size_t>(n) * d, s);
+    o.alloc(n, s);
+    HM_CUDA(cudaMemcpyAsync(a.get(), y, sizeof(double) * n * d, cudaMemcpyHostToDevice, s));
+    HM_CUDA(cudaMemcpyAsync(b.get(), yp, sizeof(double) * n * d, cudaMemcpyHostToDevice, s));
+    eval_pairs_kernel<<<grid_for(n, 256, 1 << 16), 256, 0, s>>>(kp, d, n, a.get(), b.get(), o.get());
+    HM_LAUNCH_CHECK();
+    HM_CUDA(cudaMemcpyAsync(out, o.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+void hm_exp_port_host(int64_t n, const double* x, double* out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = glibc_exp(x[i]);
+}
+
+hm_status hm_exp_port_device(int64_t n, const double* x, double* out) {
+  return guarded([&] {
+    require_device();
+    if (n <= 0) return;
+    cudaStream_t s = nullptr;
+    DevBuf<double> a, o;
+    a.alloc(n, s);
+    o.alloc(n, s);
+    HM_CUDA(cudaMemcpyAsync(a.get(), x, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    exp_port_kernel<<<grid_for(n, 256, 1 << 16), 256, 0, s>>>(n, a.get(), o.get());
+    HM_LAUNCH_CHECK();
+    HM_CUDA(cudaMemcpyAsync(out, o.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,112 @@
+// hmatrix.h -- device-resident H-matrix state and the host orchestration of
+// setup() and mvp() (reference: proj/include/hmat/hmatrix.hpp:36-59).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+#include "kernel_math.cuh"
+
+namespace hmb {
+
+struct Config {
+  double eta = 1.5;
+  long long c_leaf = 256;
+  long long k = 16;
+  long long bs_aca = 1ll << 20;
+  long long bs_dense = 1ll << 22;
+  bool precompute_aca = false;
+  bool has_epsilon = false;
+  double epsilon = 0.0;
+  int mode = 0;          // 0 geometric, 1 force dense, 2 force admissible
+  int near_stored = 0;   // 0: near field recomputed per product (reference), 1: stored at setup
+  int rank = 0, world = 1;
+  long long aca_chunk_rows = 0;  // recompute-mode workspace cap in rows (0 = automatic)
+};
+
+// One leaf list (dense or admissible), canonical order (tree.cpp:189-194).
+struct LeafList {
+  long long count = 0;
+  DevBuf<int> rl, m, cl, n;  // row.lower, |row|, col.lower, |col|
+  DevBuf<int> tau_slot;      // cluster-table slot of the row cluster
+  DevBuf<int> sigma_slot;
+  DevBuf<unsigned char> depth;
+  // per cluster slot: [start, end) of the run of leaves with that row cluster
+  DevBuf<int> run_start, run_end;
+  std::vector<int> h_rl, h_m, h_cl, h_n;  // host mirrors (small; used for partitioning)
+};
+
+struct Timings {
+  double morton_ms = 0, tree_ms = 0, aca_ms = 0, near_ms = 0, setup_ms = 0;
+  double mvp_ms = 0, mvp_dense_ms = 0, mvp_aca_ms = 0;
+};
+
+struct HMatrix {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  Config cfg;
+  KernelParams kp{};
+  long long n = 0;
+  int d = 0;
+
+  // points (Morton order, SoA) and permutation: slot i holds original point perm[i]
+  DevBuf<double> coords;
+  DevBuf<long long> perm;
+  DevBuf<unsigned long long> codes;  // Morton codes in input order (introspection)
+
+  // implicit cluster tree: slot = depth_base[e] + idx, e in [0, dcap]
+  int dcap = 0;       // deepest depth with boxes
+  int dmax_leaf = 0;  // deepest depth holding a leaf
+  std::vector<long long> depth_base;
+  long long nslots = 0;
+  DevBuf<long long> slot_lo, slot_hi;  // cluster ranges
+  DevBuf<double> boxes;                // 2*d per slot: a[0..d), b[0..d)
+
+  LeafList dense, aca;
+
+  // rows owned by this rank (Morton order), [row_begin, row_end)
+  long long row_begin = 0, row_end = 0;
+
+  // admissible-block factors: U rank-major (kmax x m), V interleaved (n x kmax)
+  DevBuf<long long> u_off, v_off;  // per aca leaf (also per-chunk in recompute mode)
+  DevBuf<double> U, V;
+  DevBuf<int> k_eff, row_piv, col_piv;
+  DevBuf<int> aca_order;    // aca leaves by size, largest first
+  DevBuf<double> t;         // per (aca leaf, rank) V^T x
+  bool factors_valid = false;
+  long long aca_rejections = 0;
+
+  // stored near field: column-major blocks
+  DevBuf<long long> dense_off;
+  DevBuf<double> dense_vals;
+
+  // product workspaces
+  DevBuf<double> xm, zm, xin, zout;
+  DevBuf<int> counter;
+
+  // algorithmic sizes
+  double S_d = 0, sum_m_adm = 0, sum_n_adm = 0, S_l = 0;
+  Timings tm;
+
+  ~HMatrix();
+};
+
+// setup() pipeline (hmatrix.cpp:38-64); coords_dev: d x n SoA on the device.
+void build_hmatrix(HMatrix& h, const double* coords_dev);
+// mvp (hmatrix.cpp:66-123) on device vectors in ORIGINAL order.
+void mvp_device(HMatrix& h, const double* x_dev, double* z_dev, cudaStream_t s);
+// Morton-ordered product into h.zm (rows [row_begin,row_end)), x already in h.xm.
+void mvp_morton(HMatrix& h, cudaStream_t s);
+
+// components
+void morton_codes_device(const double* coords, long long n, int d, unsigned long long* codes, cudaStream_t s);
+void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStream_t s);
+void store_near_field(HMatrix& h, cudaStream_t s);
+void plan_far_field(HMatrix& h, cudaStream_t s);
+// explicit-matrix ACA seam (aca.cpp:567-578) on the GPU
+void aca_dense_blocks(long long nblocks, const long long* shapes, const double* entries_host, long long kmax,
+                      bool has_eps, double eps, double eta, long long* k_eff, long long* row_piv,
+                      long long* col_piv, double* u_host, double* v_host, cudaStream_t s);
+
+
+}  // namespace hmb

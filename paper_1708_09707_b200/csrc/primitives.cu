@@ -1,0 +1,255 @@
+// primitives.cu -- exclusive scan and stable LSD radix sort (sm_100a).
+//
+// Replaces the reference's serial exclusive_scan (parallel.cpp:129-138) and
+// std::stable_sort-based stable_sort_by_key (parallel.hpp:45-62).
+#include "primitives.h"
+
+namespace hmb {
+
+namespace {
+
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ long long warp_incl_scan(long long v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan of one value per thread; returns the block total in *total.
+template <int NT>
+__device__ long long block_excl_scan(long long v, long long* smem_warp, long long* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long incl = warp_incl_scan(v);
+  if (lane == 31) smem_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    long long w = lane < NT / 32 ? smem_warp[lane] : 0;
+    w = warp_incl_scan(w);
+    if (lane < NT / 32) smem_warp[lane] = w;
+  }
+  __syncthreads();
+  const long long warp_off = warp ? smem_warp[warp - 1] : 0;
+  *total = smem_warp[NT / 32 - 1];
+  __syncthreads();
+  return warp_off + incl - v;
+}
+
+__global__ void scan_reduce_kernel(const long long* __restrict__ in, long long n, long long* __restrict__ sums) {
+  __shared__ long long sw[kScanThreads / 32];
+  const long long base = static_cast<long long>(blockIdx.x) * kScanTile;
+  long long acc = 0;
+#pragma unroll
+  for (int q = 0; q < kScanItems; ++q) {
+    const long long i = base + q * kScanThreads + threadIdx.x;
+    if (i < n) acc += in[i];
+  }
+  long long tot;
+  block_excl_scan<kScanThreads>(acc, sw, &tot);
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+// single CTA: exclusive scan of sums in place, carrying across chunks
+__global__ void scan_sums_kernel(long long* sums, long long nb, long long* grand) {
+  __shared__ long long sw[1024 / 32];
+  long long carry = 0;
+  for (long long base = 0; base < nb; base += 1024) {
+    const long long i = base + threadIdx.x;
+    const long long v = i < nb ? sums[i] : 0;
+    long long tot;
+    const long long ex = block_excl_scan<1024>(v, sw, &tot);
+    if (i < nb) sums[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) *grand = carry;
+}
+
+__global__ void scan_apply_kernel(const long long* __restrict__ in, long long* __restrict__ out, long long n,
+                                  const long long* __restrict__ sums) {
+  __shared__ long long sw[kScanThreads / 32];
+  // blocked arrangement: thread t owns items [t*8, t*8+8) of the tile
+  const long long base = static_cast<long long>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+  long long v[kScanItems];
+  long long acc = 0;
+#pragma unroll
+  for (int q = 0; q < kScanItems; ++q) {
+    v[q] = base + q < n ? in[base + q] : 0;
+    acc += v[q];
+  }
+  long long tot;
+  long long run = block_excl_scan<kScanThreads>(acc, sw, &tot) + sums[blockIdx.x];
+#pragma unroll
+  for (int q = 0; q < kScanItems; ++q) {
+    if (base + q < n) out[base + q] = run;
+    run += v[q];
+  }
+}
+
+__global__ void iota_kernel(unsigned* out, long long n) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<unsigned>(i);
+}
+
+// ---------------------------------------------------------------- radix sort
+constexpr int kSortThreads = 256;
+constexpr int kSortRounds = 8;
+constexpr int kSortTile = kSortThreads * kSortRounds;
+
+__global__ void key_and_or_kernel(const unsigned long long* __restrict__ keys, long long n,
+                                  unsigned long long* and_or) {
+  unsigned long long a = ~0ull, o = 0ull;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    a &= keys[i];
+    o |= keys[i];
+  }
+#pragma unroll
+  for (int s = 16; s; s >>= 1) {
+    a &= __shfl_xor_sync(0xffffffffu, a, s);
+    o |= __shfl_xor_sync(0xffffffffu, o, s);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAnd(&and_or[0], a);
+    atomicOr(&and_or[1], o);
+  }
+}
+
+__global__ void radix_hist_kernel(const unsigned long long* __restrict__ keys, long long n, int shift,
+                                  long long ntiles, long long* __restrict__ hist) {
+  __shared__ unsigned h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const long long base = static_cast<long long>(blockIdx.x) * kSortTile;
+#pragma unroll
+  for (int q = 0; q < kSortRounds; ++q) {
+    const long long i = base + q * kSortThreads + threadIdx.x;
+    if (i < n) atomicAdd(&h[(keys[i] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  hist[static_cast<long long>(threadIdx.x) * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void radix_scatter_kernel(const unsigned long long* __restrict__ keys, const unsigned* __restrict__ vals,
+                                     unsigned long long* __restrict__ okeys, unsigned* __restrict__ ovals, long long n,
+                                     int shift, long long ntiles, const long long* __restrict__ offs) {
+  __shared__ long long gofs[256];
+  __shared__ unsigned run[256];
+  __shared__ unsigned cnt[kSortThreads / 32][256];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  gofs[t] = offs[static_cast<long long>(t) * ntiles + blockIdx.x];
+  run[t] = 0;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const long long base = static_cast<long long>(blockIdx.x) * kSortTile;
+  for (int q = 0; q < kSortRounds; ++q) {
+#pragma unroll
+    for (int ww = 0; ww < kSortThreads / 32; ++ww) cnt[ww][t] = 0;
+    __syncthreads();
+    const long long i = base + q * kSortThreads + t;
+    const bool valid = i < n;
+    unsigned long long key = 0;
+    unsigned val = 0;
+    unsigned digit = 256;  // sentinel class for invalid lanes
+    if (valid) {
+      key = keys[i];
+      val = vals[i];
+      digit = static_cast<unsigned>((key >> shift) & 255u);
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, digit);
+    const unsigned rank = __popc(peers & lt_mask);
+    if (valid && rank == 0) cnt[w][digit] = __popc(peers);
+    __syncthreads();
+    {
+      unsigned acc = run[t];
+#pragma unroll
+      for (int ww = 0; ww < kSortThreads / 32; ++ww) {
+        const unsigned c = cnt[ww][t];
+        cnt[ww][t] = acc;
+        acc += c;
+      }
+      run[t] = acc;
+    }
+    __syncthreads();
+    if (valid) {
+      const long long dst = gofs[digit] + cnt[w][digit] + rank;
+      okeys[dst] = key;
+      ovals[dst] = val;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+long long exclusive_scan_i64(const long long* in, long long* out, long long n, cudaStream_t s) {
+  if (n <= 0) return 0;
+  const long long nb = (n + kScanTile - 1) / kScanTile;
+  DevBuf<long long> sums;
+  sums.alloc(static_cast<size_t>(nb + 1), s);
+  scan_reduce_kernel<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, n, sums.get());
+  HM_LAUNCH_CHECK();
+  scan_sums_kernel<<<1, 1024, 0, s>>>(sums.get(), nb, sums.get() + nb);
+  HM_LAUNCH_CHECK();
+  scan_apply_kernel<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, out, n, sums.get());
+  HM_LAUNCH_CHECK();
+  long long total = 0;
+  HM_CUDA(cudaMemcpyAsync(&total, sums.get() + nb, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  HM_CUDA(cudaStreamSynchronize(s));
+  return total;
+}
+
+void iota_u32(unsigned* out, long long n, cudaStream_t s) {
+  if (n <= 0) return;
+  iota_kernel<<<grid_for(n, 256, 65535), 256, 0, s>>>(out, n);
+  HM_LAUNCH_CHECK();
+}
+
+void radix_sort_pairs(unsigned long long* keys, unsigned* vals, long long n, cudaStream_t s) {
+  if (n <= 1) return;
+  DevBuf<unsigned long long> ao;
+  ao.alloc(2, s);
+  unsigned long long init[2] = {~0ull, 0ull};
+  HM_CUDA(cudaMemcpyAsync(ao.get(), init, sizeof(init), cudaMemcpyHostToDevice, s));
+  key_and_or_kernel<<<grid_for(n, 256, 4096), 256, 0, s>>>(keys, n, ao.get());
+  HM_LAUNCH_CHECK();
+  unsigned long long host_ao[2];
+  HM_CUDA(cudaMemcpyAsync(host_ao, ao.get(), sizeof(host_ao), cudaMemcpyDeviceToHost, s));
+  HM_CUDA(cudaStreamSynchronize(s));
+  const unsigned long long varying = host_ao[0] ^ host_ao[1];
+  if (!varying) return;
+
+  const long long ntiles = (n + kSortTile - 1) / kSortTile;
+  DevBuf<unsigned long long> kalt;
+  DevBuf<unsigned> valt;
+  DevBuf<long long> hist;
+  kalt.alloc(static_cast<size_t>(n), s);
+  valt.alloc(static_cast<size_t>(n), s);
+  hist.alloc(static_cast<size_t>(256 * ntiles), s);
+  unsigned long long* kin = keys;
+  unsigned* vin = vals;
+  unsigned long long* kout = kalt.get();
+  unsigned* vout = valt.get();
+  for (int shift = 0; shift < 64; shift += 8) {
+    if (((varying >> shift) & 255ull) == 0) continue;
+    radix_hist_kernel<<<static_cast<unsigned>(ntiles), kSortThreads, 0, s>>>(kin, n, shift, ntiles, hist.get());
+    HM_LAUNCH_CHECK();
+    exclusive_scan_i64(hist.get(), hist.get(), 256 * ntiles, s);
+    radix_scatter_kernel<<<static_cast<unsigned>(ntiles), kSortThreads, 0, s>>>(kin, vin, kout, vout, n, shift,
+                                                                             ntiles, hist.get());
+    HM_LAUNCH_CHECK();
+    std::swap(kin, kout);
+    std::swap(vin, vout);
+  }
+  if (kin != keys) {
+    HM_CUDA(cudaMemcpyAsync(keys, kin, sizeof(unsigned long long) * n, cudaMemcpyDeviceToDevice, s));
+    HM_CUDA(cudaMemcpyAsync(vals, vin, sizeof(unsigned) * n, cudaMemcpyDeviceToDevice, s));
+  }
+}
+
+}  // namespace hmb
