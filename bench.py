@@ -1,0 +1,356 @@
+#!/usr/bin/env python3
+"""bench.py -- H-MVP throughput of the B200 H-matrix engine (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], the metric's single-GPU config): N = 2^20 uniform
+points in [0,1]^2 (SplitMix64(42), point-major), Gaussian kernel, eta = 1.5,
+C_leaf = 64, k = 16, STORED near field and STORED low-rank factors.  One step = one
+H-matrix-vector product z = H(A) x (reference mvp(), hmatrix.cpp:66-123) with x =
+SplitMix64(43+t).symmetric() resident in HBM.  The stored operator (~80 GB) is far
+larger than the 126 MB L2, so no flush is needed between steps.
+
+  value     = 2 (S_d + S_l) / t  [GFLOP/s, algorithmic, SURVEY.md §8d], whole job
+  e2e       = same metric through hm_mvp (C ABI) with host x/z, H2D + D2H inside
+  roofline  = dominant kernel (the row-gather product kernel) vs measured HBM peak
+  build_s   = hm_setup wall time (Morton + tree + ACA factors + dense blocks)
+
+N > 1 (torchrun): rows are partitioned by depth-log2(N) row clusters,
+every rank computes its slice, NCCL allgathers y; N is fixed -> strong scaling.
+
+--impl reference: the unmodified reference library (oracle/_ref) on the host cores,
+on a bounded row sample of the same workload (see oracle/refbench.py).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "H-MVP GFLOP/s & HBM GB/s + build time (s) at N=2^20..2^24, 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=1 << 20)
+    ap.add_argument("--d", type=int, default=2)
+    ap.add_argument("--c-leaf", dest="c_leaf", type=int, default=64)
+    ap.add_argument("--k", type=int, default=16)
+    ap.add_argument("--kernel", choices=["gaussian", "matern"], default="gaussian")
+    ap.add_argument("--mode", choices=["stored", "recompute"], default="stored")
+    ap.add_argument("--cpu-baseline", dest="cpu_baseline", type=int, default=1,
+                    help="time the reference on the host cores beside the GPU number (rank 0, N=1)")
+    ap.add_argument("--cpu-workers", dest="cpu_workers", type=int, default=0)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def reference_sample(args, steps: int, warmup: int, workers: int = 0):
+    """Run oracle/refbench.py workers (one single-threaded process per core)."""
+    ncores = os.cpu_count() or 1
+    workers = workers or max(1, min(ncores, 16))
+    # leaf-level row clusters spread evenly over [0, N)
+    depth = 0
+    while ((args.n - 1) >> depth) + 1 > args.c_leaf:
+        depth += 1
+    nclusters = 1 << depth
+    ids = [int((w + 0.5) * nclusters / workers) for w in range(workers)]
+    env = dict(os.environ, HMAT_THREADS="1", PYTHONPATH=REPO)
+    procs = []
+    for w in range(workers):
+        cmd = [sys.executable, "-m", "oracle.refbench", "--n", str(args.n), "--d", str(args.d), "--c-leaf",
+               str(args.c_leaf), "--k", str(args.k), "--kernel", "1" if args.kernel == "matern" else "0",
+               "--clusters", str(ids[w]), "--reps", str(steps), "--warmup", str(warmup)]
+        procs.append(subprocess.Popen(cmd, cwd=REPO, env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                      text=True))
+    outs = []
+    for p in procs:
+        o, e = p.communicate()
+        if p.returncode != 0:
+            raise RuntimeError("reference worker failed: " + e[-2000:])
+        outs.append(json.loads(o.strip().splitlines()[-1]))
+    flops = sum(o["flops_per_rep"] * o["reps"] for o in outs)
+    t = max(o["t_mvp_ms"] for o in outs) / 1e3
+    rows = sum(o["rows"] for o in outs)
+    return {"value": flops / t / 1e9, "cores": workers, "flops": flops, "seconds": t, "rows": rows,
+            "steps": steps, "setup_s": max(o["t_setup_ms"] for o in outs) / 1e3,
+            "aca_s": max(o["t_aca_ms"] for o in outs) / 1e3,
+            "sample": f"{workers} single-thread reference processes (HMAT_THREADS=1; the pool races, SURVEY F1), "
+                      f"each one leaf row cluster ({rows} of {args.n} rows total) x {steps} products of the "
+                      f"precompute-mode mvp() body over every leaf touching those rows"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    cfg = {"workload": f"H-MVP, N=2^{args.n.bit_length() - 1} uniform [0,1]^{args.d}, {args.kernel}, eta=1.5, "
+                       f"C_leaf={args.c_leaf}, k={args.k}, reference precompute-mode mvp() on a row sample",
+           "n": args.n, "d": args.d, "gpus_requested": world}
+    try:
+        from oracle.bind import available
+        if not available("ref"):
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libhmat_ref.so was not built"}))
+            return
+        r = reference_sample(args, max(1, args.steps // 10), 1 if args.warmup else 0, args.cpu_workers)
+    except Exception as e:  # noqa: BLE001
+        print(json.dumps({"impl": "reference", "unavailable": f"reference run failed: {e}"[:300]}))
+        return
+    ms = r["seconds"] / r["steps"] * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": "GFLOP/s", "n_gpus": 0,
+            "steps": r["steps"], "warmup": 1 if args.warmup else 0, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": r["value"], "unit": "GFLOP/s", "cores": r["cores"], "kind": "reference",
+                             "sample": r["sample"]},
+            "e2e": {"value": r["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "reference_setup_s": r["setup_s"], "reference_aca_s": r["aca_s"]}
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import paper_1708_09707_b200 as hm
+    from paper_1708_09707_b200.inputs import uniform_points, symmetric
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    n, d = args.n, args.d
+    pts = uniform_points(n, d, 42)
+    stored = args.mode == "stored"
+    cfg = hm.HmatrixConfig(c_leaf=args.c_leaf, k=args.k, precompute_aca=stored, near_stored=stored, rank=rank,
+                           world=world, device=local)
+    kern = hm.KernelFunction(args.kernel)
+    t0 = time.perf_counter()
+    h = hm.setup(pts, kern, cfg)
+    build_s = time.perf_counter() - t0
+    if world > 1:
+        uid = hm.nccl_unique_id() if rank == 0 else bytes(128)
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        h.attach_nccl(obj[0])
+    st = h.stats()
+    tms = h.timings()
+
+    # algorithmic work of the WHOLE product (all ranks): flops and bytes, SURVEY.md §8d
+    def allsum(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        return float(t.item())
+
+    S_d = allsum(st["S_d_own"])
+    S_lm = allsum(st["S_lm"])
+    S_ln = allsum(st["S_ln"])
+    S_l = S_lm + S_ln
+    if not stored:  # recompute mode: S_l from a one-off factorisation for the metric only
+        f = h.aca_factors(factors=False)
+        lv = h.aca_queue
+        S_l = float((f["k_eff"] * ((lv[:, 1] - lv[:, 0]) + (lv[:, 3] - lv[:, 2]))).sum())
+        S_lm = float((f["k_eff"] * (lv[:, 1] - lv[:, 0])).sum())
+        S_ln = S_l - S_lm
+    flops = 2.0 * (S_d + S_l)
+    alg_bytes = 8.0 * (S_d + S_l + 2 * n)
+
+    # inputs resident in HBM
+    xs = [torch.from_numpy(symmetric(43 + t, n)).cuda() for t in range(4)]
+    z = torch.empty(n, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for t in range(args.warmup):
+        h.mvp_device(xs[t % 4].data_ptr(), z.data_ptr(), sptr)
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        ev0.record(stream)
+        for t in range(args.steps):
+            h.mvp_device(xs[t % 4].data_ptr(), z.data_ptr(), sptr)
+        ev1.record(stream)
+        barrier()
+    dev_ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        tt = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dev_ms = float(tt.item())
+    ms_step = dev_ms / args.steps
+    value = flops / (ms_step * 1e-3) / 1e9
+    hbm = alg_bytes / (ms_step * 1e-3) / 1e9
+
+    # per-kernel device times (dominant kernel roofline)
+    barrier()
+    h.profile_begin()
+    prof_steps = max(3, min(args.steps, 10))
+    for t in range(prof_steps):
+        h.mvp_device(xs[t % 4].data_ptr(), z.data_ptr(), sptr)
+    barrier()
+    prof = h.profile_end()
+    rows_ms, rows_cnt = prof.get("rows", (0.0, 0))
+    rows_avg = rows_ms / max(rows_cnt, 1)
+    # algorithmic bytes of the row-gather kernel on this rank: stored dense blocks + U
+    # (k_eff x m per admissible leaf) + z write; the t kernel streams V (k_eff x n)
+    rows_bytes = 8.0 * (st["S_d_own"] + st["S_lm"] + (st["row_end"] - st["row_begin"]))
+    hbm_peak, peak_kind = peaks()
+    rows_gbs = rows_bytes / (rows_avg * 1e-3) / 1e9 if rows_avg > 0 else None
+    launches_per_step = sum(c for (_, c) in prof.values()) / prof_steps
+
+    # end to end through the C ABI with host buffers (H2D + D2H inside)
+    x_host = [symmetric(43 + t, n) for t in range(4)]
+    barrier()
+    e2e_steps = max(3, args.steps // 2)
+    h.mvp(x_host[0])
+    barrier()
+    te = time.perf_counter()
+    for t in range(e2e_steps):
+        h.mvp(x_host[t % 4])
+    barrier()
+    e2e_s = (time.perf_counter() - te) / e2e_steps
+    if world > 1:
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e_value = flops / e2e_s / 1e9
+
+    # check the product against the oracle on a few rows?  (tests/ do that; the bench
+    # only reports a checksum so runs can be compared)
+    zc = z.double().cpu().numpy()
+    checksum = float(np.sqrt(np.sum(zc * zc)))
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and args.cpu_baseline:
+            try:
+                r = reference_sample(args, 3, 1, args.cpu_workers)
+                cpu = {"value": r["value"], "unit": "GFLOP/s", "cores": r["cores"], "kind": "reference",
+                       "sample": r["sample"]}
+            except Exception as e:  # noqa: BLE001
+                cpu = {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "reference",
+                       "sample": f"failed: {e}"[:300]}
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"H-MVP on a stored H-matrix: N=2^{n.bit_length() - 1} uniform points in [0,1]^{d}"
+                                   f" (SplitMix64(42)), {args.kernel}, eta=1.5, C_leaf={args.c_leaf}, k={args.k}, "
+                                   f"{args.mode} near/far field, x=SplitMix64(43+t)",
+                       "n": n, "d": d, "c_leaf": args.c_leaf, "k": args.k, "mode": args.mode,
+                       "parallelism": f"row-cluster x{world}" if world > 1 else "single",
+                       "l2": f"no flush: stored operator {alg_bytes / 1e9:.1f} GB >> 126 MB L2"},
+            "hbm_gbs": hbm, "build_s": build_s,
+            "build_phases_ms": {k: tms[k] for k in ("morton_ms", "tree_ms", "aca_ms", "near_ms", "setup_ms")},
+            "work": {"S_d": S_d, "S_l": S_l, "S_lm": S_lm, "S_ln": S_ln, "flops_per_step": flops,
+                     "alg_bytes_per_step": alg_bytes, "n_dense": st["n_dense"], "n_aca": st["n_aca"],
+                     "aca_rejections": st["aca_rejections"]},
+            "roofline": {"bound": "hbm", "kernel": "rows_kernel (near+far row gather)",
+                         "achieved": rows_gbs, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": (rows_gbs / hbm_peak) if rows_gbs else None, "traffic": None,
+                         "peak_kind": peak_kind, "alg_bytes_per_launch": rows_bytes, "avg_ms": rows_avg},
+            "kernels_ms_per_step": {k: v[0] / max(v[1], 1) * (v[1] / prof_steps) for k, v in prof.items()},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
+            "gpu_launches": int(round(launches_per_step * args.steps)),
+            "clocks": clocks.summary(),
+            "checksum_norm_z": checksum,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -70,6 +70,8 @@ typedef struct {
 typedef struct {
   int64_t n_dense, n_aca;
   double S_d, S_l, sum_m_adm, sum_n_adm;
+  double S_lm, S_ln;       /* sum_adm k_eff*m and k_eff*n (own rows, precompute mode) */
+  double S_d_own;          /* dense entries of the rows this rank owns */
   int64_t aca_rejections;  /* rejected candidate columns in the last factorisation */
   int32_t dmax_leaf;
   int64_t row_begin, row_end;
@@ -107,6 +109,13 @@ hm_status hm_relative_error(hm_handle* h, const double* x, double* out);
 /* exact dense product z = A x (oracle.cpp:24-55 semantics, device), original ordering */
 hm_status hm_dense_mvp(hm_handle* h, const double* x, double* z);
 
+/* Per-kernel device timing: CUDA events recorded on the launching stream around
+ * every launch between begin and end; end returns the summed milliseconds and launch
+ * counts per kernel id (0 gather x, 1 V^T x, 2 near+far rows, 3 scatter z,
+ * 4 ACA (recompute mode), 5 far-field rows (recompute mode), 6 y allgather, 7 unused). */
+hm_status hm_profile_begin(hm_handle* h);
+hm_status hm_profile_end(hm_handle* h, double ms[8], int64_t counts[8]);
+
 /* ---- introspection for bit-exact parity checks ---- */
 hm_status hm_get_stats(hm_handle* h, hm_stats* st);
 hm_status hm_get_timings(hm_handle* h, hm_timings* t);
@@ -139,6 +148,9 @@ hm_status hm_eval_kernel(int32_t kernel, double matern_beta, int32_t d, int64_t 
 void hm_exp_port_host(int64_t n, const double* x, double* out);
 /* Device glibc-exp port. */
 hm_status hm_exp_port_device(int64_t n, const double* x, double* out);
+/* glibc-log ports (Matern K1 series, core.cpp:46), host and device. */
+void hm_log_port_host(int64_t n, const double* x, double* out);
+hm_status hm_log_port_device(int64_t n, const double* x, double* out);
 
 #ifdef __cplusplus
 }

@@ -10,6 +10,7 @@
 // The reference worker pool races with more than one thread (SURVEY.md F1,
 // parallel.cpp:33-92), so the constructor below pins HMAT_THREADS=1 unless the
 // caller set it explicitly.
+#include <chrono>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -375,6 +376,69 @@ int ref_mvp_rows(void* h, const double* x, std::int64_t nranges, const std::int6
         for (std::int64_t i = 0; i < batch.items[b].row.size(); ++i) z_morton[batch.items[b].row.lower + i] += y[batch.row_offset[b] + i];
       }
     }
+  });
+}
+
+// Bench sample for the reference CPU arm: the leaves touching the given row ranges
+// are factorised first (aca_batched, the precompute_aca=true path of setup(),
+// hmatrix.cpp:57-62; reported as t_aca_ms) and then `reps` products are timed with
+// the reference's precompute-mode mvp() body (dense assemble + gemv, low-rank apply,
+// hmatrix.cpp:80-113; t_mvp_ms is the total).  flops = 2*(sum_dense m*n +
+// sum_adm k_eff*(m+n)) of the evaluated leaves per product.
+int ref_mvp_rows_timed(void* h, const double* x, std::int64_t nranges, const std::int64_t* ranges, std::int64_t reps,
+                       double* z_morton, double* t_aca_ms, double* t_mvp_ms, double* flops) {
+  return guarded([&] {
+    using Clock = std::chrono::steady_clock;
+    const RefHandle* r = static_cast<RefHandle*>(h);
+    const std::int64_t n = r->h.points.count;
+    const auto hit = [&](const WorkItem& w) {
+      for (std::int64_t q = 0; q < nranges; ++q) {
+        if (w.row.lower < ranges[2 * q + 1] && ranges[2 * q] < w.row.upper) return true;
+      }
+      return false;
+    };
+    std::vector<WorkItem> dense, aca;
+    for (const WorkItem& w : r->h.dense_queue) if (hit(w)) dense.push_back(w);
+    for (const WorkItem& w : r->h.aca_queue) if (hit(w)) aca.push_back(w);
+    AcaOptions opt;
+    opt.max_rank = r->h.config.k;
+    opt.epsilon = r->h.config.epsilon;
+    opt.eta = r->h.config.eta;
+    const auto t0 = Clock::now();
+    const std::vector<AcaBatch> batches = partition_aca_queue(aca, r->h.config.bs_aca);
+    std::vector<BatchedAcaResult> factors;
+    for (const AcaBatch& b : batches) factors.push_back(aca_batched(b, r->kernel, r->h.points, opt));
+    *t_aca_ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+    double f = 0.0;
+    for (const WorkItem& w : dense) f += 2.0 * static_cast<double>(w.row.size()) * static_cast<double>(w.col.size());
+    for (std::size_t gi = 0; gi < batches.size(); ++gi)
+      for (std::size_t b = 0; b < batches[gi].items.size(); ++b)
+        f += 2.0 * static_cast<double>(factors[gi].k_eff[b]) *
+             static_cast<double>(batches[gi].items[b].row.size() + batches[gi].items[b].col.size());
+    *flops = f;
+    const std::vector<DenseGroup> groups = partition_dense_queue(dense, r->h.config.bs_dense);
+    const auto t1 = Clock::now();
+    for (std::int64_t rep = 0; rep < reps; ++rep) {
+      const std::vector<double> xm = permute_vector({x, static_cast<std::size_t>(n)}, r->h.points.perm, PermDirection::Forward);
+      std::fill(z_morton, z_morton + n, 0.0);
+      DenseBatch dbatch;
+      std::vector<double> y;
+      for (const DenseGroup& g : groups) {
+        assemble_dense_batch(g, r->kernel, r->h.points, dbatch);
+        gather_dense_inputs(dbatch, xm);
+        batched_gemv(dbatch, y);
+        for (std::size_t b = 0; b < g.items.size(); ++b)
+          for (std::int64_t i = 0; i < g.items[b].row.size(); ++i) z_morton[g.items[b].row.lower + i] += y[g.row_offset[b] + i];
+      }
+      for (std::size_t gi = 0; gi < batches.size(); ++gi) {
+        const AcaBatch& batch = batches[gi];
+        y.assign(static_cast<std::size_t>(batch.total_rows), 0.0);
+        batched_low_rank_apply(factors[gi], batch, xm, y);
+        for (std::size_t b = 0; b < batch.items.size(); ++b)
+          for (std::int64_t i = 0; i < batch.items[b].row.size(); ++i) z_morton[batch.items[b].row.lower + i] += y[batch.row_offset[b] + i];
+      }
+    }
+    *t_mvp_ms = std::chrono::duration<double, std::milli>(Clock::now() - t1).count();
   });
 }
 

@@ -73,7 +73,7 @@ class _Timings(C.Structure):
 
 class _Stats(C.Structure):
     _fields_ = [("n_dense", _i64), ("n_aca", _i64), ("S_d", _d), ("S_l", _d), ("sum_m_adm", _d),
-                ("sum_n_adm", _d), ("aca_rejections", _i64), ("dmax_leaf", _i32), ("row_begin", _i64),
+                ("sum_n_adm", _d), ("S_lm", _d), ("S_ln", _d), ("S_d_own", _d), ("aca_rejections", _i64), ("dmax_leaf", _i32), ("row_begin", _i64),
                 ("row_end", _i64), ("device_bytes", _d)]
 
 
@@ -109,14 +109,20 @@ _sig("hm_aca_dense", C.c_int, [_i64, _p, _p, _i64, _i32, _d, _d, _p, _p, _p, _p,
 _sig("hm_eval_kernel", C.c_int, [_i32, _d, _i32, _i64, _p, _p, _p])
 _sig("hm_exp_port_host", None, [_i64, _p, _p])
 _sig("hm_exp_port_device", C.c_int, [_i64, _p, _p])
+_sig("hm_profile_begin", C.c_int, [_p])
+_sig("hm_profile_end", C.c_int, [_p, _p, _p])
+_sig("hm_log_port_host", None, [_i64, _p, _p])
+_sig("hm_log_port_device", C.c_int, [_i64, _p, _p])
 
 EXPORTED_SYMBOLS = [
     "hm_last_error", "hm_config_default", "hm_device_count", "hm_setup", "hm_setup_device", "hm_destroy",
     "hm_mvp", "hm_mvp_device", "hm_nccl_unique_id", "hm_attach_nccl", "hm_cg_solve", "hm_relative_error",
     "hm_dense_mvp", "hm_get_stats", "hm_get_timings", "hm_get_points", "hm_get_codes", "hm_get_leaves",
     "hm_get_aca", "hm_morton_codes", "hm_morton_order", "hm_aca_dense", "hm_eval_kernel", "hm_exp_port_host",
-    "hm_exp_port_device",
+    "hm_exp_port_device", "hm_log_port_host", "hm_log_port_device", "hm_profile_begin", "hm_profile_end",
 ]
+
+KERNEL_IDS = ["gather_x", "lowrank_t", "rows", "scatter_z", "aca", "rows_far", "allgather", "unused"]
 
 
 def _check(rc: int) -> None:
@@ -256,6 +262,16 @@ class HMatrix:
     def attach_nccl(self, unique_id: bytes) -> None:
         buf = (C.c_ubyte * 128).from_buffer_copy(unique_id)
         _check(_lib.hm_attach_nccl(self._h, buf))
+
+    # --- per-kernel device timing (CUDA events on the launching stream)
+    def profile_begin(self) -> None:
+        _check(_lib.hm_profile_begin(self._h))
+
+    def profile_end(self) -> dict:
+        ms = np.zeros(8)
+        cnt = np.zeros(8, dtype=np.int64)
+        _check(_lib.hm_profile_end(self._h, _ptr(ms), _ptr(cnt)))
+        return {name: (float(ms[i]), int(cnt[i])) for i, name in enumerate(KERNEL_IDS) if cnt[i]}
 
     # --- introspection
     def stats(self) -> dict:
@@ -433,6 +449,20 @@ def exp_port_device(x) -> np.ndarray:
     x = np.ascontiguousarray(x, dtype=np.float64)
     out = np.empty_like(x)
     _check(_lib.hm_exp_port_device(x.size, _ptr(x), _ptr(out)))
+    return out
+
+
+def log_port_host(x) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    _lib.hm_log_port_host(x.size, _ptr(x), _ptr(out))
+    return out
+
+
+def log_port_device(x) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    _check(_lib.hm_log_port_device(x.size, _ptr(x), _ptr(out)))
     return out
 
 

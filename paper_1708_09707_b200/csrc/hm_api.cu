@@ -24,6 +24,7 @@ struct hm_handle {
   HMatrix h;
   std::mutex mu;
   ncclComm_t comm = nullptr;
+  std::vector<long long> rank_bounds;  // Morton row slice [b[r], b[r+1]) of every rank
 };
 
 namespace {
@@ -158,10 +159,10 @@ __global__ void eval_pairs_kernel(KernelParams kp, int d, long long n, const dou
   }
 }
 
-__global__ void exp_port_kernel(long long n, const double* x, double* out) {
+__global__ void exp_port_kernel(long long n, const double* x, double* out, int which) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
-    out[i] = glibc_exp(x[i]);
+    out[i] = which == 0 ? glibc_exp(x[i]) : glibc_log(x[i]);
 }
 
 // exact product, one thread per Morton row, acc += phi(i,j) * x_m[j] sequentially
@@ -259,21 +260,17 @@ double device_dot(const double* a, const double* b, long long n, DevBuf<double>&
 void product(hm_handle* H, const double* x_dev, double* z_dev, cudaStream_t s) {
   HMatrix& h = H->h;
   const long long n = h.n;
+  h.clk.start(kKGather, s);
   gather_kernel<<<grid_for(n, 256, 1 << 16), 256, 0, s>>>(x_dev, h.perm.get(), n, h.xm.get());
   HM_LAUNCH_CHECK();
+  h.clk.stop(kKGather, s);
   mvp_morton(h, s);
   if (h.cfg.world > 1) {
     if (!H->comm) raise(kEnccl, "world > 1 but no NCCL communicator attached (hm_attach_nccl)");
-    // each rank's Morton row slice is broadcast in place (slices are contiguous, sizes may differ)
-    std::vector<long long> bounds(h.cfg.world + 1);
-    int g = 0;
-    while ((1 << g) < h.cfg.world) ++g;
-    for (int r = 0; r <= h.cfg.world; ++r) {
-      long long v = n;
-      if (r < h.cfg.world)
-        HM_CUDA(cudaMemcpy(&v, h.slot_lo.get() + h.depth_base[g] + r, sizeof(long long), cudaMemcpyDeviceToHost));
-      bounds[r] = v;
-    }
+    // y allgather: each rank's Morton row slice is broadcast in place;
+    // slices are contiguous and may differ in size by the ceil splits.
+    const std::vector<long long>& bounds = H->rank_bounds;
+    h.clk.start(kKAllgather, s);
     if (ncclGroupStart() != ncclSuccess) raise(kEnccl, "ncclGroupStart");
     for (int r = 0; r < h.cfg.world; ++r) {
       double* p = h.zm.get() + bounds[r];
@@ -282,9 +279,12 @@ void product(hm_handle* H, const double* x_dev, double* z_dev, cudaStream_t s) {
         raise(kEnccl, "ncclBroadcast of the y slice failed");
     }
     if (ncclGroupEnd() != ncclSuccess) raise(kEnccl, "ncclGroupEnd");
+    h.clk.stop(kKAllgather, s);
   }
+  h.clk.start(kKScatter, s);
   scatter_kernel<<<grid_for(n, 256, 1 << 16), 256, 0, s>>>(h.zm.get(), h.perm.get(), n, z_dev);
   HM_LAUNCH_CHECK();
+  h.clk.stop(kKScatter, s);
 }
 
 }  // namespace
@@ -401,9 +401,46 @@ hm_status hm_attach_nccl(hm_handle* H, const unsigned char id[128]) {
   return guarded([&] {
     ncclUniqueId u;
     std::memcpy(&u, id, 128);
-    HM_CUDA(cudaSetDevice(H->h.device));
-    if (ncclCommInitRank(&H->comm, H->h.cfg.world, u, H->h.cfg.rank) != ncclSuccess)
+    HMatrix& h = H->h;
+    HM_CUDA(cudaSetDevice(h.device));
+    if (ncclCommInitRank(&H->comm, h.cfg.world, u, h.cfg.rank) != ncclSuccess)
       raise(kEnccl, "ncclCommInitRank failed");
+    int g = 0;
+    while ((1 << g) < h.cfg.world) ++g;
+    H->rank_bounds.assign(h.cfg.world + 1, h.n);
+    HM_CUDA(cudaMemcpy(H->rank_bounds.data(), h.slot_lo.get() + h.depth_base[g], sizeof(long long) * h.cfg.world,
+                       cudaMemcpyDeviceToHost));
+  });
+}
+
+hm_status hm_profile_begin(hm_handle* H) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lock(H->mu);
+    H->h.clk.on = true;
+  });
+}
+
+hm_status hm_profile_end(hm_handle* H, double* ms, int64_t* counts) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lock(H->mu);
+    KClock& c = H->h.clk;
+    c.on = false;
+    for (int id = 0; id < kKNum; ++id) {
+      double acc = 0.0;
+      const size_t cnt = std::min(c.ev[id][0].size(), c.ev[id][1].size());
+      for (size_t i = 0; i < cnt; ++i) {
+        HM_CUDA(cudaEventSynchronize(c.ev[id][1][i]));
+        float t = 0.f;
+        HM_CUDA(cudaEventElapsedTime(&t, c.ev[id][0][i], c.ev[id][1][i]));
+        acc += t;
+      }
+      if (ms) ms[id] = acc;
+      if (counts) counts[id] = static_cast<int64_t>(cnt);
+      for (int w = 0; w < 2; ++w) {
+        for (cudaEvent_t e : c.ev[id][w]) cudaEventDestroy(e);
+        c.ev[id][w].clear();
+      }
+    }
   });
 }
 
@@ -534,6 +571,9 @@ hm_status hm_get_stats(hm_handle* H, hm_stats* st) {
     st->S_l = h.S_l;
     st->sum_m_adm = h.sum_m_adm;
     st->sum_n_adm = h.sum_n_adm;
+    st->S_lm = h.S_lm;
+    st->S_ln = h.S_ln;
+    st->S_d_own = h.S_d_own;
     st->aca_rejections = h.aca_rejections;
     st->dmax_leaf = h.dmax_leaf;
     st->row_begin = h.row_begin;
@@ -730,7 +770,16 @@ void hm_exp_port_host(int64_t n, const double* x, double* out) {
   for (int64_t i = 0; i < n; ++i) out[i] = glibc_exp(x[i]);
 }
 
-hm_status hm_exp_port_device(int64_t n, const double* x, double* out) {
+void hm_log_port_host(int64_t n, const double* x, double* out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = glibc_log(x[i]);
+}
+
+static hm_status libm_port_device(int which, int64_t n, const double* x, double* out);
+
+hm_status hm_exp_port_device(int64_t n, const double* x, double* out) { return libm_port_device(0, n, x, out); }
+hm_status hm_log_port_device(int64_t n, const double* x, double* out) { return libm_port_device(1, n, x, out); }
+
+static hm_status libm_port_device(int which, int64_t n, const double* x, double* out) {
   return guarded([&] {
     require_device();
     if (n <= 0) return;
@@ -739,7 +788,7 @@ hm_status hm_exp_port_device(int64_t n, const double* x, double* out) {
     a.alloc(n, s);
     o.alloc(n, s);
     HM_CUDA(cudaMemcpyAsync(a.get(), x, sizeof(double) * n, cudaMemcpyHostToDevice, s));
-    exp_port_kernel<<<grid_for(n, 256, 1 << 16), 256, 0, s>>>(n, a.get(), o.get());
+    exp_port_kernel<<<grid_for(n, 256, 1 << 16), 256, 0, s>>>(n, a.get(), o.get(), which);
     HM_LAUNCH_CHECK();
     HM_CUDA(cudaMemcpyAsync(out, o.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
     HM_CUDA(cudaStreamSynchronize(s));

@@ -36,6 +36,25 @@ struct LeafList {
   std::vector<int> h_rl, h_m, h_cl, h_n;  // host mirrors (small; used for partitioning)
 };
 
+// Per-kernel CUDA-event clock (enabled by hm_profile_begin): events are recorded on
+// the launching stream around each launch and summed at hm_profile_end.
+enum KernelId : int {
+  kKGather = 0, kKLowrankT = 1, kKRows = 2, kKScatter = 3, kKAca = 4, kKRowsFar = 5, kKAllgather = 6, kKNum = 8
+};
+struct KClock {
+  bool on = false;
+  std::vector<cudaEvent_t> ev[kKNum][2];
+  void mark(int id, int which, cudaStream_t s) {
+    if (!on) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, s);
+    ev[id][which].push_back(e);
+  }
+  void start(int id, cudaStream_t s) { mark(id, 0, s); }
+  void stop(int id, cudaStream_t s) { mark(id, 1, s); }
+};
+
 struct Timings {
   double morton_ms = 0, tree_ms = 0, aca_ms = 0, near_ms = 0, setup_ms = 0;
   double mvp_ms = 0, mvp_dense_ms = 0, mvp_aca_ms = 0;
@@ -85,8 +104,10 @@ struct HMatrix {
   DevBuf<int> counter;
 
   // algorithmic sizes
-  double S_d = 0, sum_m_adm = 0, sum_n_adm = 0, S_l = 0;
+  double S_d = 0, sum_m_adm = 0, sum_n_adm = 0, S_l = 0, S_lm = 0, S_ln = 0;
+  double S_d_own = 0;  // dense entries of the rows this rank owns
   Timings tm;
+  KClock clk;
 
   ~HMatrix();
 };

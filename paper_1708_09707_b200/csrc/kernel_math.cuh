@@ -5,12 +5,12 @@
 //   Matern:    r2 == 0 ? norm : K1(r)*r*norm  core.cpp:130-134, r = sqrt(r2)
 //   r2 = ((0 + dx0*dx0) + dx1*dx1) + ...     core.hpp:103-110 (axis order, no FMA)
 //
-// The Gaussian is bit-exact with the reference (glibc_exp.h).  The Matern path
-// uses IEEE sqrt/div exactly like the reference but CUDA's log() for the K1
-// series term (glibc's log is not ported yet), so Matern entries may differ by
-// an ulp from the host; DESIGN.md states this.
+// Both kernels are bit-exact with the reference: exp and log are ports of the
+// glibc FMA variants (glibc_exp.h, glibc_log.h), sqrt/div are IEEE, and no
+// product/sum is contracted.
 #pragma once
 #include "glibc_exp.h"
+#include "glibc_log.h"
 
 namespace hmb {
 
@@ -22,13 +22,7 @@ struct KernelParams {
   double matern_norm;  // 1 / (2^(beta-1) Gamma(beta)), computed on the host with glibc pow/tgamma
 };
 
-HM_HD double hm_log(double x) {
-#ifdef __CUDA_ARCH__
-  return log(x);
-#else
-  return std::log(x);
-#endif
-}
+HM_HD double hm_log(double x) { return glibc_log(x); }
 HM_HD double hm_sqrt(double x) {
 #ifdef __CUDA_ARCH__
   return __dsqrt_rn(x);

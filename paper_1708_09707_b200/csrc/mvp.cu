@@ -385,8 +385,12 @@ void plan_far_field(HMatrix& h, cudaStream_t s) {
     std::vector<int> ke(hi - lo);
     if (hi > lo) HM_CUDA(cudaMemcpyAsync(ke.data(), h.k_eff.get() + lo, sizeof(int) * (hi - lo), cudaMemcpyDeviceToHost, s));
     HM_CUDA(cudaStreamSynchronize(s));
-    h.S_l = 0;
-    for (long long b = lo; b < hi; ++b) h.S_l += static_cast<double>(ke[b - lo]) * (h.aca.h_m[b] + h.aca.h_n[b]);
+    h.S_l = h.S_lm = h.S_ln = 0;
+    for (long long b = lo; b < hi; ++b) {
+      h.S_lm += static_cast<double>(ke[b - lo]) * h.aca.h_m[b];
+      h.S_ln += static_cast<double>(ke[b - lo]) * h.aca.h_n[b];
+    }
+    h.S_l = h.S_lm + h.S_ln;
   }
 }
 
@@ -409,15 +413,21 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
     HM_CUDA(cudaMemcpyAsync(&vb, h.v_off.get() + alo, sizeof(long long), cudaMemcpyDeviceToHost, s));
     HM_CUDA(cudaStreamSynchronize(s));
     // aca_order covers [alo, ahi) from the precompute
+    h.clk.start(kKLowrankT, s);
     launch_t(h, ahi - alo, vb, s);
+    h.clk.stop(kKLowrankT, s);
     a.a_ubase = ub;
     a.a_lo = alo;
     a.a_hi = ahi;
+    h.clk.start(kKRows, s);
     dispatch_rows(h, a, near, true, s);
+    h.clk.stop(kKRows, s);
     return;
   }
   // recompute mode (reference default): near field first, then ACA chunk by chunk
+  h.clk.start(kKRows, s);
   dispatch_rows(h, a, near, false, s);
+  h.clk.stop(kKRows, s);
   const long long kmax = h.cfg.k;
   // chunk budget: U+V bytes
   size_t free_b = 0, total_b = 0;
@@ -442,14 +452,20 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
     HM_CUDA(cudaStreamSynchronize(s));
     if (h.U.size() < static_cast<size_t>(ue - ub)) h.U.alloc(ue - ub, s);
     if (h.V.size() < static_cast<size_t>(ve - vb)) h.V.alloc(ve - vb, s);
+    h.clk.start(kKAca, s);
     compute_aca(h, c0, c1, s);
+    h.clk.stop(kKAca, s);
+    h.clk.start(kKLowrankT, s);
     launch_t(h, c1 - c0, vb, s);
+    h.clk.stop(kKLowrankT, s);
     RowArgs b = base_row_args(h);
     b.z_in = h.zm.get();
     b.a_ubase = ub;
     b.a_lo = c0;
     b.a_hi = c1;
+    h.clk.start(kKRowsFar, s);
     dispatch_rows(h, b, 0, true, s);
+    h.clk.stop(kKRowsFar, s);
     c0 = c1;
   }
 }

@@ -550,6 +550,10 @@ void build_hmatrix(HMatrix& h, const double* coords_in) {
     h.row_begin = 0;
     h.row_end = n;
   }
+  h.S_d_own = 0;
+  for (long long i = 0; i < h.dense.count; ++i)
+    if (h.dense.h_rl[i] >= h.row_begin && h.dense.h_rl[i] < h.row_end)
+      h.S_d_own += static_cast<double>(h.dense.h_m[i]) * h.dense.h_n[i];
   h.tm.setup_ms = ms_since(t_setup);
 }
 

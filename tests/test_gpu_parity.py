@@ -2,9 +2,8 @@
 
 Bars: Morton codes, permutation, sorted coordinates, leaf lists,
 admissibility flags and boxes bit-exact; ACA pivots, k_eff and factors bit-exact
-for the Gaussian (glibc-exact exp); the H-MVP bitwise equal to the single-thread
-reference order (which also meets the <=1e-8 rel-l2 bar).  Matern entries use
-CUDA's log (not glibc's), so Matern factors/products are checked to 1e-12.
+(glibc-exact exp and log ports, no FMA contraction); the H-MVP bitwise equal to
+the single-thread reference order (which implies the <=1e-8 rel-l2 bar).
 """
 import numpy as np
 import pytest
@@ -76,17 +75,13 @@ def test_aca_pivots_and_factors(built, n, d, c_leaf, kind):
     P, h, o = built(n, d, c_leaf, kind)
     fh = h.aca_factors()
     fo = o.aca_all()
-    if kind == 0:
-        assert np.array_equal(fh["k_eff"], fo["k_eff"])
-        assert np.array_equal(fh["row_piv"], fo["row_piv"])
-        assert np.array_equal(fh["col_piv"], fo["col_piv"])
-        for a, b in zip(fh["u"], fo["u"]):
-            assert np.array_equal(bits(a), bits(b))
-        for a, b in zip(fh["v"], fo["v"]):
-            assert np.array_equal(bits(a), bits(b))
-    else:
-        agree = np.mean(np.all(fh["row_piv"] == fo["row_piv"], axis=1))
-        assert agree > 0.99
+    assert np.array_equal(fh["k_eff"], fo["k_eff"])
+    assert np.array_equal(fh["row_piv"], fo["row_piv"])
+    assert np.array_equal(fh["col_piv"], fo["col_piv"])
+    for a, b in zip(fh["u"], fo["u"]):
+        assert np.array_equal(bits(a), bits(b))
+    for a, b in zip(fh["v"], fo["v"]):
+        assert np.array_equal(bits(a), bits(b))
 
 
 @pytest.mark.parametrize("n,d,c_leaf,kind", CASES)
@@ -97,10 +92,7 @@ def test_mvp_matches_reference_order(built, n, d, c_leaf, kind, mode):
     x = symmetric(7, n)
     zh = h.mvp(x)
     zo = o.mvp(x)
-    if kind == 0:
-        assert np.array_equal(bits(zh), bits(zo)), f"max |dz| = {np.max(np.abs(zh - zo))}"
-    else:
-        assert rel_l2(zh, zo) <= 1e-12
+    assert np.array_equal(bits(zh), bits(zo)), f"max |dz| = {np.max(np.abs(zh - zo))}, rel {rel_l2(zh, zo)}"
 
 
 def test_c1_norm_anchor(built):
@@ -126,6 +118,37 @@ def test_exp_port_device_bitwise(gpu):
     want = np.frompyfunc(libm.exp, 1, 1)(xs).astype(np.float64)
     with np.errstate(invalid="ignore"):
         assert np.array_equal(bits(got), bits(want))
+
+
+def test_log_port_device_bitwise(gpu):
+    import ctypes
+    libm = ctypes.CDLL("libm.so.6")
+    libm.log.restype = ctypes.c_double
+    libm.log.argtypes = [ctypes.c_double]
+    rng = np.random.default_rng(2)
+    xs = np.concatenate([rng.uniform(0, 1, 300_000), rng.uniform(0.9, 1.1, 200_000), np.exp(rng.uniform(-700, 700, 50_000)),
+                         np.array([0.0, 1.0, np.inf, 5e-324, 1e-310, 0.9375, 1.064697265625, 0.5, 2.0])])
+    got = gpu.log_port_device(xs)
+    with np.errstate(all="ignore"):
+        want = np.frompyfunc(libm.log, 1, 1)(xs).astype(np.float64)
+    assert np.array_equal(bits(got), bits(want))
+
+
+def test_kernel_entries_bitwise(gpu, oracle):
+    rng = np.random.default_rng(3)
+    for d in (1, 2, 3, 4, 7):
+        y = rng.uniform(0, 1, (d, 20000))
+        yp = rng.uniform(0, 1, (d, 20000))
+        yp[:, :50] = y[:, :50]  # coincident points: r2 == 0 branch
+        for kind, name in ((0, "gaussian"), (1, "matern")):
+            got = gpu.eval_kernel(gpu.KernelFunction(name), y, yp)
+            want = oracle.eval_kernel(kind, 0.0, y, yp)
+            assert np.array_equal(bits(got), bits(want)), (d, name)
+    # the continued-fraction branch (r > 2): points outside [0,1]^d
+    y = rng.uniform(0, 5, (3, 5000))
+    yp = rng.uniform(0, 5, (3, 5000))
+    assert np.array_equal(bits(gpu.eval_kernel(gpu.KernelFunction("matern"), y, yp)),
+                          bits(oracle.eval_kernel(1, 0.0, y, yp)))
 
 
 def test_explicit_seam_matches_oracle(gpu, oracle):
