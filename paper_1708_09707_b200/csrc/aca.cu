@@ -92,6 +92,7 @@ struct AcaJob {
   double eps_factor;        // eps (1 - eta) / (1 + eps), aca.cpp:49
   int* counter;
   unsigned long long* rejections;
+  int tile_shift;           // -1: U rank-major; else log2(S), U row-tiled by S rows
   // explicit-matrix seam: block b entries at dense + dense_off[b], row-major m x n
   const double* dense;
   const long long* dense_off;
@@ -127,9 +128,16 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaJob J, KernelEntry<
     const int b = J.order[job];
     const int rl = J.rl[b], m = J.m[b], cl = J.cl[b], n = J.nn[b];
     const int kmax = J.kmax;
-    double* U = J.U + (J.u_off[b] - J.u_base);  // kmax x m, rank-major
+    double* U = J.U + (J.u_off[b] - J.u_base);  // kmax x m: rank-major, or row-tiled (tile_shift >= 0)
     double* V = J.V + (J.v_off[b] - J.v_base);  // n x kmax, interleaved
     const double* A = DENSE ? J.dense + J.dense_off[b] : nullptr;
+    // U element (l, i): rank-major l*m + i, or tiled [i / S][l][i % S] so that the
+    // k x S slice of one row tile is contiguous for the product's bulk copies
+    const int tsh = J.tile_shift;
+    auto uix = [&](int l, int i) -> long long {
+      if (tsh < 0) return static_cast<long long>(l) * m + i;
+      return ((static_cast<long long>(i >> tsh) * kmax + l) << tsh) + (i & ((1 << tsh) - 1));
+    };
 
     int G = 32;
     while (G < m && G < kAcaThreads) G <<= 1;
@@ -168,7 +176,6 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaJob J, KernelEntry<
         const bool valid = c < n;
         double sum = 0.0, bv = -1.0;
         int bi = 0x7fffffff;
-        double* buf = col_in_smem ? s_col + g * m : U + static_cast<long long>(r) * m;
         if (valid) {
           for (int i = lt; i < m; i += G) {
             double a;
@@ -179,8 +186,9 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaJob J, KernelEntry<
               E.load(rl + i, y);
               a = E.eval(y, cl + c);
             }
-            for (int l = 0; l < r; ++l) a = hsub(a, hmul(U[static_cast<long long>(l) * m + i], s_vj[g][l]));
-            buf[i] = a;
+            for (int l = 0; l < r; ++l) a = hsub(a, hmul(U[uix(l, i)], s_vj[g][l]));
+            if (col_in_smem) s_col[g * m + i] = a;
+            else U[uix(r, i)] = a;
             sum = hadd(sum, hmul(a, a));
             bool used = false;
             for (int l = 0; l < r; ++l) used |= (s_piv[l] == i);
@@ -230,9 +238,9 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaJob J, KernelEntry<
                 } else if (hi <= T) {
                   q = false;
                 } else {  // ambiguous: the reference's sequential fold (aca.cpp:373-374 / 414-415)
-                  const double* cb = col_in_smem ? s_col + gg * m : U + static_cast<long long>(r) * m;
-                  double f = hmul(cb[0], cb[0]);
-                  for (int i = 1; i < m; ++i) f = hadd(f, hmul(cb[i], cb[i]));
+                  auto cbv = [&](int i) { return col_in_smem ? s_col[gg * m + i] : U[uix(r, i)]; };
+                  double f = hmul(cbv(0), cbv(0));
+                  for (int i = 1; i < m; ++i) f = hadd(f, hmul(cbv(i), cbv(i)));
                   q = f > T;
                 }
               }
@@ -260,18 +268,17 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaJob J, KernelEntry<
 
       // ---------------- accepted column: pivot, normalise, pivot-row pass
       const int ga = s_acc, cstar = s_next, p = s_prow;
-      const double* cb = col_in_smem ? s_col + ga * m : U + static_cast<long long>(r) * m;
+      auto cbv = [&](int i) { return col_in_smem ? s_col[ga * m + i] : U[uix(r, i)]; };
       if (r == 0 && tid == 0) {
         // scale2 = exact left fold of the first accepted column (aca.cpp:491)
-        double f = hmul(cb[0], cb[0]);
-        for (int i = 1; i < m; ++i) f = hadd(f, hmul(cb[i], cb[i]));
+        double f = hmul(cbv(0), cbv(0));
+        for (int i = 1; i < m; ++i) f = hadd(f, hmul(cbv(i), cbv(i)));
         s_scale = f;
       }
-      const double pivot_val = cb[p];
-      for (int l = tid; l < r; l += kAcaThreads) s_upiv[l] = U[static_cast<long long>(l) * m + p];
+      const double pivot_val = cbv(p);
+      for (int l = tid; l < r; l += kAcaThreads) s_upiv[l] = U[uix(l, p)];
       __syncthreads();
-      for (int i = tid; i < m; i += kAcaThreads)
-        U[static_cast<long long>(r) * m + i] = __ddiv_rn(cb[i], pivot_val);
+      for (int i = tid; i < m; i += kAcaThreads) U[uix(r, i)] = __ddiv_rn(cbv(i), pivot_val);
       {
         double yp[DIM > 0 ? DIM : 20];
         if constexpr (!DENSE) E.load(rl + p, yp);
@@ -295,16 +302,15 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaJob J, KernelEntry<
       if (J.has_eps) {
         // epsilon criterion with the reference's exact left folds (aca.cpp:497-538); test path
         if (tid == 0) {
-          const double* ur = U + static_cast<long long>(r) * m;
-          double nu = hmul(ur[0], ur[0]);
-          for (int i = 1; i < m; ++i) nu = hadd(nu, hmul(ur[i], ur[i]));
+          auto ur = [&](int i) { return U[uix(r, i)]; };
+          double nu = hmul(ur(0), ur(0));
+          for (int i = 1; i < m; ++i) nu = hadd(nu, hmul(ur(i), ur(i)));
           double nv = hmul(V[r], V[r]);
           for (int j = 1; j < n; ++j) nv = hadd(nv, hmul(V[static_cast<long long>(j) * kmax + r], V[static_cast<long long>(j) * kmax + r]));
           double cross = 0.0;
           for (int l = 0; l < r; ++l) {
-            const double* ul = U + static_cast<long long>(l) * m;
-            double du = hmul(ul[0], ur[0]);
-            for (int i = 1; i < m; ++i) du = hadd(du, hmul(ul[i], ur[i]));
+            double du = hmul(U[uix(l, 0)], ur(0));
+            for (int i = 1; i < m; ++i) du = hadd(du, hmul(U[uix(l, i)], ur(i)));
             double dv = hmul(V[l], V[r]);
             for (int j = 1; j < n; ++j)
               dv = hadd(dv, hmul(V[static_cast<long long>(j) * kmax + l], V[static_cast<long long>(j) * kmax + r]));
@@ -343,8 +349,10 @@ __global__ void size_key_kernel(const int* __restrict__ m, const int* __restrict
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < cnt;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long b = begin + i;
-    const unsigned long long work = static_cast<unsigned long long>(m[b]) + static_cast<unsigned long long>(nn[b]);
-    keys[i] = ~work & 0xffffffffull;  // largest first
+    // n descending, then m descending: largest first, and the n >= 2048 blocks of the
+    // low-rank apply form a prefix
+    keys[i] = ((~static_cast<unsigned long long>(nn[b]) & 0xffffffffull) << 32) |
+              (~static_cast<unsigned long long>(m[b]) & 0xffffffffull);
     vals[i] = static_cast<unsigned>(b);
   }
 }
@@ -365,6 +373,8 @@ void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStrea
                                                                keys.get(), reinterpret_cast<unsigned*>(h.aca_order.get()));
   HM_LAUNCH_CHECK();
   radix_sort_pairs(keys.get(), reinterpret_cast<unsigned*>(h.aca_order.get()), cnt, s);
+  h.aca_long_jobs = 0;
+  for (long long b = leaf_begin; b < leaf_end; ++b) h.aca_long_jobs += h.aca.h_n[b] >= 2048 ? 1 : 0;
   h.counter.alloc(1, s);
   h.counter.zero(s);
   DevBuf<unsigned long long> rej;
@@ -395,6 +405,7 @@ void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStrea
   J.eps_factor = h.cfg.epsilon * (1.0 - h.cfg.eta) / (1.0 + h.cfg.epsilon);
   J.counter = h.counter.get();
   J.rejections = rej.get();
+  J.tile_shift = h.u_tile_shift;
   switch (h.d) {
     case 1: launch_kernel_aca<1>(J, h, s); break;
     case 2: launch_kernel_aca<2>(J, h, s); break;
@@ -473,6 +484,7 @@ void aca_dense_blocks(long long nb, const long long* shapes, const double* entri
   J.has_eps = has_eps ? 1 : 0;
   J.eps_factor = eps * (1.0 - eta) / (1.0 + eps);
   J.counter = cnt.get();
+  J.tile_shift = -1;
   J.dense = dA.get();
   J.dense_off = ddo.get();
   KernelEntry<1> E{nullptr, 0, 1, KernelParams{0, 1, 0.0}};

@@ -115,7 +115,8 @@ void setup_common(hm_handle* H, const double* coords_dev, long long n, int d) {
       if (static_cast<long long>(h.dense.h_m[b]) * h.dense.h_n[b] > h.cfg.bs_dense)
         raise(kEinval, "partition_dense_queue: a single block exceeds bs_dense");
   }
-  h.xm.alloc(n, h.stream);
+  h.xm.alloc(n + 16, h.stream);  // padded: bulk copies round x segments up to 16 bytes
+  h.xm.zero(h.stream);
   h.zm.alloc(n, h.stream);
   h.zm.zero(h.stream);
   const auto ta = Clock::now();
@@ -137,6 +138,9 @@ hm_handle* new_handle(const hm_config* cfg, long long n, int d, int kernel, doub
   H->h.device = cfg ? cfg->device : 0;
   HM_CUDA(cudaSetDevice(H->h.device));
   HM_CUDA(cudaStreamCreateWithFlags(&H->h.stream, cudaStreamNonBlocking));
+  HM_CUDA(cudaStreamCreateWithFlags(&H->h.aux, cudaStreamNonBlocking));
+  HM_CUDA(cudaEventCreateWithFlags(&H->h.ev_fork, cudaEventDisableTiming));
+  HM_CUDA(cudaEventCreateWithFlags(&H->h.ev_join, cudaEventDisableTiming));
   H->h.kp = make_kernel(kernel, beta, d);
   H->h.n = n;
   H->h.d = d;
@@ -350,13 +354,18 @@ void hm_destroy(hm_handle* H) {
   if (!H) return;
   cudaSetDevice(H->h.device);
   if (H->comm) ncclCommDestroy(H->comm);
-  cudaStream_t s = H->h.stream;
+  cudaStream_t s = H->h.stream, aux = H->h.aux;
+  cudaEvent_t e0 = H->h.ev_fork, e1 = H->h.ev_join;
   cudaStreamSynchronize(s);
+  if (aux) cudaStreamSynchronize(aux);
   delete H;  // buffers are freed on the stream
   if (s) {
     cudaStreamSynchronize(s);
     cudaStreamDestroy(s);
   }
+  if (aux) cudaStreamDestroy(aux);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
 }
 
 hm_status hm_mvp(hm_handle* H, const double* x, double* z, hm_timings* t) {
@@ -679,8 +688,13 @@ hm_status hm_get_aca(hm_handle* H, int64_t* k_eff, int64_t* row_piv, int64_t* co
         row_piv[b * kmax + l] = hrp[b * kmax + l];
         col_piv[b * kmax + l] = hcp[b * kmax + l];
         const bool live = l < hk[b];
+        const int sh = h.factors_valid ? h.u_tile_shift : -1;
         if (u)
-          for (long long i = 0; i < m; ++i) u[uo[b] + l * m + i] = live ? hu[uo[b] + l * m + i] : 0.0;
+          for (long long i = 0; i < m; ++i) {
+            const long long src =
+                sh < 0 ? l * m + i : ((((i >> sh) * kmax) + l) << sh) + (i & ((1ll << sh) - 1));
+            u[uo[b] + l * m + i] = live ? hu[uo[b] + src] : 0.0;
+          }
         if (v)
           for (long long j = 0; j < n; ++j) v[vo[b] + l * n + j] = live ? hv[vo[b] + j * kmax + l] : 0.0;
       }

@@ -83,14 +83,29 @@ struct HMatrix {
 
   LeafList dense, aca;
 
+  // Per deepest-level row cluster c (depth dmax_leaf): the leaf runs of every cluster of
+  // its ancestor chain, in canonical order (tree.cpp:189-194), as CSR spans [start, end)
+  // into the dense / aca lists.  All rows of c accumulate exactly these leaves, in order.
+  DevBuf<int> row_cluster;             // Morton row -> deepest cluster index
+  DevBuf<int> dspan_ptr, aspan_ptr;    // size 2^dmax_leaf + 1
+  DevBuf<int> dspans, aspans;          // (start, end) pairs
+
   // rows owned by this rank (Morton order), [row_begin, row_end)
   long long row_begin = 0, row_end = 0;
 
   // admissible-block factors: U rank-major (kmax x m), V interleaved (n x kmax)
   DevBuf<long long> u_off, v_off;  // per aca leaf (also per-chunk in recompute mode)
   DevBuf<double> U, V;
+  // Regular geometry (N = S * 2^dmax_leaf, S a power of two <= 256, k even) with stored
+  // factors: U is row-tiled by S rows ([i/S][l][i%S]) and the product runs the
+  // TMA-pipelined cluster kernel; otherwise U is rank-major (kmax x m).
+  int u_tile_shift = -1;
+  bool tma_rows = false;
   DevBuf<int> k_eff, row_piv, col_piv;
-  DevBuf<int> aca_order;    // aca leaves by size, largest first
+  DevBuf<int> aca_order;    // aca leaves by column count n, largest first
+  long long aca_long_jobs = 0;  // prefix of aca_order with n >= 2048 (CTA-per-block fold path)
+  cudaStream_t aux = nullptr;   // auxiliary stream (long folds run beside the short ones)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DevBuf<double> t;         // per (aca leaf, rank) V^T x
   bool factors_valid = false;
   long long aca_rejections = 0;

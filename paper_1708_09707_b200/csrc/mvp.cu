@@ -24,7 +24,7 @@ namespace hmb {
 
 namespace {
 
-constexpr int kMaxDepth = 32;
+
 
 __global__ void gather_x_kernel(const double* __restrict__ x, const long long* __restrict__ perm, long long n,
                                 double* __restrict__ xm) {
@@ -136,30 +136,20 @@ struct RowArgs {
   const double* t;
   int kmax;
   long long a_lo, a_hi;
+  // canonical leaf spans per deepest row cluster
+  const int* row_cluster;
+  const int* dspan_ptr;
+  const int* dspans;
+  const int* aspan_ptr;
+  const int* aspans;
 };
 
 template <int DIM, int NEAR /*0 none, 1 recompute, 2 stored*/, bool FAR>
 __global__ void __launch_bounds__(256) rows_kernel(RowArgs a) {
   const long long i = a.row_begin + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (i >= a.row_end) return;
-  // chain of clusters containing row i: slot of depth e = 2^e - 1 + idx_e
-  long long lo_e[kMaxDepth];
-  long long slot_e[kMaxDepth];
-  {
-    long long lo = 0, hi = a.n, idx = 0;
-    for (int e = 0; e <= a.dmax; ++e) {
-      lo_e[e] = lo;
-      slot_e[e] = ((1ll << e) - 1) + idx;
-      const long long mid = lo + (hi - lo + 1) / 2;
-      if (i < mid) {
-        hi = mid;
-        idx = 2 * idx;
-      } else {
-        lo = mid;
-        idx = 2 * idx + 1;
-      }
-    }
-  }
+  // leaves of row i, in canonical order, are the CSR spans of its deepest cluster
+  const int c = __ldg(a.row_cluster + i);
   double yi[DIM > 0 ? DIM : 20];
   if constexpr (NEAR == 1) {
     if constexpr (DIM > 0) {
@@ -171,17 +161,11 @@ __global__ void __launch_bounds__(256) rows_kernel(RowArgs a) {
   }
   double z = a.z_in ? a.z_in[i] : 0.0;
 
-  // canonical order of the chain: groups of equal row.lower ascending; inside a group
-  // the deeper (smaller row.upper) cluster first
   if constexpr (NEAR != 0) {
-    for (int e0 = 0; e0 <= a.dmax;) {
-      int e1 = e0;
-      while (e1 + 1 <= a.dmax && lo_e[e1 + 1] == lo_e[e0]) ++e1;
-      for (int e = e1; e >= e0; --e) {
-        const long long s = slot_e[e];
-        const int rs = a.d_rs[s];
-        if (rs < 0) continue;
-        const int re = a.d_re[s];
+    const int p1 = __ldg(a.dspan_ptr + c + 1);
+    for (int p = __ldg(a.dspan_ptr + c); p < p1; ++p) {
+      {
+        const int rs = __ldg(a.dspans + 2 * p), re = __ldg(a.dspans + 2 * p + 1);
         for (int L = rs; L < re; ++L) {
           const int r0 = a.d_rl[L], mb = a.d_m[L], c0 = a.d_cl[L], nb = a.d_n[L];
           const double* x = a.xm + c0;
@@ -221,33 +205,230 @@ __global__ void __launch_bounds__(256) rows_kernel(RowArgs a) {
           z = hadd(z, y);
         }
       }
-      e0 = e1 + 1;
     }
   }
   if constexpr (FAR) {
-    for (int e0 = 0; e0 <= a.dmax;) {
-      int e1 = e0;
-      while (e1 + 1 <= a.dmax && lo_e[e1 + 1] == lo_e[e0]) ++e1;
-      for (int e = e1; e >= e0; --e) {
-        const long long s = slot_e[e];
-        int rs = a.a_rs[s];
-        if (rs < 0) continue;
-        int re = a.a_re[s];
-        rs = static_cast<int>(max(static_cast<long long>(rs), a.a_lo));
-        re = static_cast<int>(min(static_cast<long long>(re), a.a_hi));
-        for (int L = rs; L < re; ++L) {
-          const int r0 = a.a_rl[L], mb = a.a_m[L], ke = a.a_keff[L];
-          const double* u = a.U + (a.a_uoff[L] - a.a_ubase) + (i - r0);
-          const double* tl = a.t + static_cast<long long>(L) * a.kmax;
-          double y = 0.0;
-          for (int l = 0; l < ke; ++l) y = hadd(y, hmul(__ldcs(u + static_cast<long long>(l) * mb), __ldg(tl + l)));
-          z = hadd(z, y);
+    const int p1 = __ldg(a.aspan_ptr + c + 1);
+    for (int p = __ldg(a.aspan_ptr + c); p < p1; ++p) {
+      const int rs = static_cast<int>(max(static_cast<long long>(__ldg(a.aspans + 2 * p)), a.a_lo));
+      const int re = static_cast<int>(min(static_cast<long long>(__ldg(a.aspans + 2 * p + 1)), a.a_hi));
+      for (int L = rs; L < re; ++L) {
+        const int r0 = __ldg(a.a_rl + L), mb = __ldg(a.a_m + L), ke = __ldg(a.a_keff + L);
+        const double* u = a.U + (__ldg(a.a_uoff + L) - a.a_ubase) + (i - r0);
+        const double* tl = a.t + static_cast<long long>(L) * a.kmax;
+        // y = ((0 + u_0 t_0) + u_1 t_1) + ...  (aca.cpp:609-616); loads issued ahead of the fold
+        double y = 0.0;
+        for (int l0 = 0; l0 < ke; l0 += 8) {
+          double uv[8], tv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const bool ok = l0 + q < ke;
+            uv[q] = ok ? __ldcs(u + static_cast<long long>(l0 + q) * mb) : 0.0;
+            tv[q] = ok ? __ldg(tl + l0 + q) : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (l0 + q < ke) y = hadd(y, hmul(uv[q], tv[q]));
         }
+        z = hadd(z, y);
       }
-      e0 = e1 + 1;
     }
   }
   a.z_out[i] = z;
+}
+
+// ---------------------------------------------------------------------------------
+// TMA-pipelined product for regular geometry (N = S * 2^D): one CTA of S threads per
+// deepest row cluster c (rows [cS, cS+S)), one thread per row.  Every leaf touching c
+// contributes one contiguous chunk -- the S x n dense block (column-major) or the
+// k_eff x S tile of U -- plus its x segment or t vector; a single elected thread
+// streams these chunks with cp.async.bulk (TMA) into a ring of shared-memory stages
+// tracked by mbarriers, so the HBM stream never waits on the sequential folds.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes));
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity));
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct TmaArgs {
+  RowArgs r;
+  int D;
+  const int* a_tslot;   // aca leaf -> row-cluster slot
+};
+
+// Item cursor over the dense spans (column chunks of CW) then the aca spans of
+// cluster c; walked only by the producer thread.
+struct ItemCursor {
+  int p, p_end, L, L_end;  // span index / leaf index within the current span
+  int j0;                  // first column of the current dense chunk
+  bool far;
+};
+
+// S rows per cluster (= CTA size), CW columns (or ranks) per item, NST ring stages.
+template <int S, int CW, int NST>
+__global__ void __launch_bounds__(S) rows_tma_kernel(TmaArgs A) {
+  __shared__ __align__(128) double sdata[NST][S * CW];
+  __shared__ __align__(16) double saux[NST][CW];
+  __shared__ __align__(8) unsigned long long bars[NST];
+  __shared__ int sdesc[NST];  // bit 9 valid, bit 8 leaf done, bits 0-7 count
+  const RowArgs& a = A.r;
+  const long long c = static_cast<long long>(blockIdx.x) + a.row_begin / S;
+  const int tid = threadIdx.x;
+
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  ItemCursor k;
+  bool done_issuing = false;
+  auto settle = [&]() -> bool {
+    for (;;) {
+      if (k.p < k.p_end && k.L < k.L_end) return true;
+      if (k.p < k.p_end) {
+        ++k.p;
+        if (k.p < k.p_end) {
+          const int* sp = k.far ? a.aspans : a.dspans;
+          k.L = __ldg(sp + 2 * k.p);
+          k.L_end = __ldg(sp + 2 * k.p + 1);
+          continue;
+        }
+      }
+      if (k.far) return false;
+      k.far = true;
+      k.p = __ldg(a.aspan_ptr + c);
+      k.p_end = __ldg(a.aspan_ptr + c + 1);
+      k.L = k.L_end = 0;
+      if (k.p < k.p_end) {
+        k.L = __ldg(a.aspans + 2 * k.p);
+        k.L_end = __ldg(a.aspans + 2 * k.p + 1);
+      }
+    }
+  };
+  // thread 0: put the next item (or the end sentinel) into stage st
+  auto issue = [&](int st) {
+    if (done_issuing) return;
+    if (!settle()) {
+      sdesc[st] = 0;
+      done_issuing = true;
+      asm volatile("{\n .reg .b64 t;\n mbarrier.arrive.shared::cta.b64 t, [%0];\n}\n" ::"r"(smem_u32(&bars[st]))
+                   : "memory");
+      return;
+    }
+    const int L = k.L;
+    if (!k.far) {
+      const int nb = __ldg(a.d_n + L);
+      const int cnt = min(CW, nb - k.j0);
+      const bool last = k.j0 + CW >= nb;
+      sdesc[st] = 512 | (last ? 256 : 0) | cnt;
+      const unsigned bytes = static_cast<unsigned>(S) * cnt * 8u;
+      const unsigned xb = static_cast<unsigned>((cnt + 1) & ~1) * 8u;
+      mbar_expect_tx(&bars[st], bytes + xb);
+      bulk_g2s(sdata[st], a.d_vals + (__ldg(a.d_off + L) - a.d_off_base) + static_cast<long long>(k.j0) * S, bytes,
+               &bars[st]);
+      bulk_g2s(saux[st], a.xm + __ldg(a.d_cl + L) + k.j0, xb, &bars[st]);
+      if (last) {
+        k.j0 = 0;
+        ++k.L;
+      } else {
+        k.j0 += CW;
+      }
+    } else {
+      const int ke = __ldg(a.a_keff + L);
+      const int ts = __ldg(A.a_tslot + L);
+      const int e = 31 - __clz(ts + 1);
+      const long long tidx = ts - ((1 << e) - 1);
+      const long long q = c - (tidx << (A.D - e));  // row tile of c inside the leaf's row cluster
+      const int ke2 = (ke + 1) & ~1;                // 16-byte multiple (k is even, t is k-strided)
+      sdesc[st] = 512 | 256 | ke;
+      if (ke2 == 0) {
+        asm volatile("{\n .reg .b64 t;\n mbarrier.arrive.shared::cta.b64 t, [%0];\n}\n" ::"r"(
+                         smem_u32(&bars[st]))
+                     : "memory");
+      } else {
+        mbar_expect_tx(&bars[st], static_cast<unsigned>(ke2) * (S + 1) * 8u);
+        bulk_g2s(sdata[st], a.U + (__ldg(a.a_uoff + L) - a.a_ubase) + q * a.kmax * S,
+                 static_cast<unsigned>(ke2) * S * 8u, &bars[st]);
+        bulk_g2s(saux[st], a.t + static_cast<long long>(L) * a.kmax, static_cast<unsigned>(ke2) * 8u, &bars[st]);
+      }
+      ++k.L;
+    }
+  };
+
+  if (tid == 0) {
+    k.far = false;
+    k.j0 = 0;
+    k.p = __ldg(a.dspan_ptr + c);
+    k.p_end = __ldg(a.dspan_ptr + c + 1);
+    k.L = k.L_end = 0;
+    if (k.p < k.p_end) {
+      k.L = __ldg(a.dspans + 2 * k.p);
+      k.L_end = __ldg(a.dspans + 2 * k.p + 1);
+    }
+#pragma unroll
+    for (int st = 0; st < NST; ++st) issue(st);
+  }
+  double z = 0.0, y = 0.0;
+  int st = 0;
+  unsigned ph = 0;
+  for (;;) {
+    mbar_wait(&bars[st], ph);
+    const int desc = sdesc[st];
+    if (!(desc & 512)) break;
+    const int cnt = desc & 255;
+    const double* dd = sdata[st] + tid;
+    const double* da = saux[st];
+    // dense: ((0 + a_0 x_0) + a_1 x_1) + ... (dense_blocks.cpp:114); far: ((0 + u_0 t_0) + ...) (aca.cpp:616)
+    if (cnt == CW) {
+      double av[CW], xv[CW];
+#pragma unroll
+      for (int q = 0; q < CW; ++q) {
+        av[q] = dd[q * S];
+        xv[q] = da[q];
+      }
+#pragma unroll
+      for (int q = 0; q < CW; ++q) y = hadd(y, hmul(av[q], xv[q]));
+    } else {
+      for (int q = 0; q < cnt; ++q) y = hadd(y, hmul(dd[q * S], da[q]));
+    }
+    if (desc & 256) {
+      z = hadd(z, y);
+      y = 0.0;
+    }
+    __syncthreads();  // stage st consumed by every thread
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(st);
+    }
+    if (++st == NST) {
+      st = 0;
+      ph ^= 1u;
+    }
+  }
+  a.z_out[c * S + tid] = z;
 }
 
 template <int DIM>
@@ -308,18 +489,371 @@ RowArgs base_row_args(HMatrix& h) {
   a.U = h.U.get();
   a.t = h.t.get();
   a.kmax = static_cast<int>(h.cfg.k);
+  a.row_cluster = h.row_cluster.get();
+  a.dspan_ptr = h.dspan_ptr.get();
+  a.dspans = h.dspans.get();
+  a.aspan_ptr = h.aspan_ptr.get();
+  a.aspans = h.aspans.get();
   return a;
+}
+
+// ---------------------------------------------------------------------------------
+// t[b, l] = v_l . x_sigma for every admissible leaf, with the reference's sequential
+// left fold (aca.cpp:613-614).  Each warp owns a ring of NST shared-memory stages and
+// pulls leaves from a largest-first queue; lane 0 streams CH-row chunks of V (n x k,
+// contiguous) and the matching x segment with cp.async.bulk, lanes l < k_eff fold
+// from shared memory.  The fold is a dependent chain, so throughput comes from the
+// many warps in flight and the critical path is the longest leaf (~5 cycles/row).
+template <int CH, int NST, int WARPS, bool DYN>
+__global__ void __launch_bounds__(WARPS * 32) t_fold_kernel(const int* __restrict__ order, long long njobs,
+                                                            const int* __restrict__ cl, const int* __restrict__ nn,
+                                                            const int* __restrict__ k_eff,
+                                                            const long long* __restrict__ v_off, long long v_base,
+                                                            const double* __restrict__ V,
+                                                            const double* __restrict__ xm, int kmax,
+                                                            int* __restrict__ counter, double* __restrict__ t) {
+  extern __shared__ __align__(128) unsigned char tf_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int stage_v = CH * kmax;          // doubles of V per stage
+  const int stage_x = CH + 2;             // doubles of x per stage (aligned-down start)
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(tf_smem) + warp * NST;
+  int* desc = reinterpret_cast<int*>(tf_smem + 8 * WARPS * NST) + warp * NST * 4;
+  double* sv = reinterpret_cast<double*>(tf_smem + 8 * WARPS * NST + 16 * WARPS * NST) +
+               static_cast<long long>(warp) * NST * (stage_v + stage_x);
+  if (lane == 0) {
+    for (int q = 0; q < NST; ++q) mbar_init(&bars[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+
+  // producer state (lane 0): current leaf and its metadata
+  int pb = -1, pn = 0, pj = 0, pke = 0;
+  long long pcl = 0, pvo = 0;
+  long long next_job = static_cast<long long>(blockIdx.x) * WARPS + warp;
+  bool pend = false;
+  auto issue = [&](int st) {
+    int* d = desc + 4 * st;
+    for (;;) {
+      if (pend) {
+        d[0] = -1;
+        asm volatile("{\n .reg .b64 t;\n mbarrier.arrive.shared::cta.b64 t, [%0];\n}\n" ::"r"(smem_u32(&bars[st]))
+                     : "memory");
+        return;
+      }
+      if (pb < 0) {
+        // short leaves: static interleaved assignment over the largest-first order (no
+        // atomics on the producer's path); long leaves: dynamic largest-first (LPT)
+        long long job;
+        if (DYN) {
+          job = atomicAdd(counter, 1);
+        } else {
+          job = next_job;
+          next_job += static_cast<long long>(gridDim.x) * WARPS;
+        }
+        if (job >= njobs) {
+          pend = true;
+          continue;
+        }
+        pb = order[job];
+        pn = nn[pb];
+        pke = k_eff[pb];
+        pcl = cl[pb];
+        pvo = v_off[pb] - v_base;
+        pj = 0;
+      }
+      break;
+    }
+    const int b = pb;
+    double* dv = sv + static_cast<long long>(st) * (stage_v + stage_x);
+    double* dx = dv + stage_v;
+    if (pke == 0) {  // rank-0 leaf: no data, t = 0
+      d[0] = b;
+      d[1] = 0;
+      d[2] = 0;
+      d[3] = 3;  // first | last, k_eff 0
+      pb = -1;
+      asm volatile("{\n .reg .b64 t;\n mbarrier.arrive.shared::cta.b64 t, [%0];\n}\n" ::"r"(smem_u32(&bars[st]))
+                   : "memory");
+      return;
+    }
+    const int cnt = min(CH, pn - pj);
+    const long long xs = pcl + pj;
+    const long long xa = xs & ~1ll;                       // 16-byte aligned start
+    const int xoff = static_cast<int>(xs - xa);
+    const int xcnt = (xoff + cnt + 1) & ~1;
+    d[0] = b;
+    d[1] = cnt;
+    d[2] = xoff;
+    d[3] = (pj == 0 ? 1 : 0) | (pj + cnt == pn ? 2 : 0) | (pke << 2);
+    const unsigned vb = static_cast<unsigned>(cnt) * kmax * 8u;
+    mbar_expect_tx(&bars[st], vb + xcnt * 8u);
+    bulk_g2s(dv, V + pvo + static_cast<long long>(pj) * kmax, vb, &bars[st]);
+    bulk_g2s(dx, xm + xa, xcnt * 8u, &bars[st]);
+    pj += cnt;
+    if (pj == pn) pb = -1;
+  };
+
+  if (lane == 0)
+    for (int st = 0; st < NST; ++st) issue(st);
+  __syncwarp();
+  double acc = 0.0;
+  int st = 0;
+  unsigned ph = 0;
+  for (;;) {
+    mbar_wait(&bars[st], ph);
+    const int* d = desc + 4 * st;
+    const int b = d[0];
+    if (b < 0) break;
+    const int cnt = d[1], xoff = d[2], flags = d[3];
+    const int ke = flags >> 2;
+    const double* dv = sv + static_cast<long long>(st) * (stage_v + stage_x);
+    const double* dx = dv + stage_v + xoff;
+    if (lane < ke) {
+      int q0 = 0;
+      if (flags & 1) {
+        acc = hmul(dv[lane], dx[0]);  // t = v_0 x_0 (aca.cpp:613)
+        q0 = 1;
+      }
+      // sub-blocks of 16 rows: loads issued ahead of the dependent adds
+      int q = q0;
+      for (; q + 16 <= cnt; q += 16) {
+        double vv[16], xx[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          vv[u] = dv[(q + u) * kmax + lane];
+          xx[u] = dx[q + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) acc = hadd(acc, hmul(vv[u], xx[u]));
+      }
+      for (; q < cnt; ++q) acc = hadd(acc, hmul(dv[q * kmax + lane], dx[q]));
+    }
+    if ((flags & 2) && lane < kmax) t[static_cast<long long>(b) * kmax + lane] = lane < ke ? acc : 0.0;
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(st);
+    }
+    __syncwarp();
+    if (++st == NST) {
+      st = 0;
+      ph ^= 1u;
+    }
+  }
+}
+
+// k == 16 specialisation of the fold: a warp folds TWO leaves at once (lanes 0-15 leaf
+// A, 16-31 leaf B; consecutive leaves of the n-descending order have equal n), with
+// constant strides, so every lane works and each stage moves 2 x CH x 16 x 8 bytes.
+template <int CH, int NST, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) t_pair_kernel(const int* __restrict__ order, long long njobs,
+                                                            const int* __restrict__ cl, const int* __restrict__ nn,
+                                                            const int* __restrict__ k_eff,
+                                                            const long long* __restrict__ v_off, long long v_base,
+                                                            const double* __restrict__ V,
+                                                            const double* __restrict__ xm, int* __restrict__ counter,
+                                                            double* __restrict__ t) {
+  constexpr int KM = 16;
+  constexpr int SV = CH * KM;      // doubles of one leaf's V chunk
+  constexpr int SX = CH + 2;       // doubles of one leaf's x chunk
+  constexpr int STAGE = 2 * SV + 2 * SX;
+  extern __shared__ __align__(128) unsigned char tp_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = lane >> 4, l = lane & 15;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(tp_smem) + warp * NST;
+  int* desc = reinterpret_cast<int*>(tp_smem + 8 * WARPS * NST) + warp * NST * 8;
+  double* sv = reinterpret_cast<double*>(tp_smem + 8 * WARPS * NST + 32 * WARPS * NST) +
+               static_cast<long long>(warp) * NST * STAGE;
+  if (lane == 0) {
+    for (int q = 0; q < NST; ++q) mbar_init(&bars[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+
+  // producer (lane 0): current pair of leaves (b[1] < 0: single leaf)
+  int pb[2] = {-1, -1}, pke[2] = {0, 0};
+  int pn = 0, pj = 0;
+  long long pcl[2] = {0, 0}, pvo[2] = {0, 0};
+  bool pend = false;
+  auto issue = [&](int st) {
+    int* d = desc + 8 * st;
+    if (pb[0] < 0 && !pend) {
+      const long long job = 2ll * atomicAdd(counter, 1);
+      if (job >= njobs) {
+        pend = true;
+      } else {
+        pb[0] = order[job];
+        pb[1] = job + 1 < njobs ? order[job + 1] : -1;
+        pn = nn[pb[0]];
+        if (pb[1] >= 0 && nn[pb[1]] != pn) {
+          // unequal lengths (size boundary): give the second leaf back as a single later
+          // -- simplest: process both as singles, A now, B next
+        }
+        for (int q = 0; q < 2; ++q)
+          if (pb[q] >= 0) {
+            pke[q] = k_eff[pb[q]];
+            pcl[q] = cl[pb[q]];
+            pvo[q] = v_off[pb[q]] - v_base;
+          }
+        pj = 0;
+      }
+    }
+    if (pend) {
+      d[0] = -1;
+      asm volatile("{\n .reg .b64 t;\n mbarrier.arrive.shared::cta.b64 t, [%0];\n}\n" ::"r"(smem_u32(&bars[st]))
+                   : "memory");
+      return;
+    }
+    // a pair is folded jointly only while both have rows left at the same offset
+    const bool pair = pb[1] >= 0 && nn[pb[1]] == pn;
+    const int cnt = min(CH, pn - pj);
+    double* dv = sv + static_cast<long long>(st) * STAGE;
+    unsigned bytes = 0;
+    int xoff[2] = {0, 0};
+    const int nl = pair ? 2 : 1;
+    for (int q = 0; q < nl; ++q) bytes += pke[q] > 0 ? static_cast<unsigned>(cnt) * KM * 8u : 0u;
+    for (int q = 0; q < nl; ++q) {
+      if (pke[q] == 0) continue;
+      const long long xs = pcl[q] + pj, xa = xs & ~1ll;
+      xoff[q] = static_cast<int>(xs - xa);
+      bytes += static_cast<unsigned>((xoff[q] + cnt + 1) & ~1) * 8u;
+    }
+    d[0] = pb[0];
+    d[1] = pair ? pb[1] : -1;
+    d[2] = cnt;
+    d[3] = xoff[0];
+    d[4] = xoff[1];
+    d[5] = (pj == 0 ? 1 : 0) | (pj + cnt == pn ? 2 : 0);
+    d[6] = pke[0];
+    d[7] = pair ? pke[1] : 0;
+    if (bytes == 0) {
+      asm volatile("{\n .reg .b64 t;\n mbarrier.arrive.shared::cta.b64 t, [%0];\n}\n" ::"r"(smem_u32(&bars[st]))
+                   : "memory");
+    } else {
+      mbar_expect_tx(&bars[st], bytes);
+      for (int q = 0; q < nl; ++q) {
+        if (pke[q] == 0) continue;
+        bulk_g2s(dv + q * SV, V + pvo[q] + static_cast<long long>(pj) * KM, static_cast<unsigned>(cnt) * KM * 8u,
+                 &bars[st]);
+        const long long xa = (pcl[q] + pj) & ~1ll;
+        bulk_g2s(dv + 2 * SV + q * SX, xm + xa, static_cast<unsigned>((xoff[q] + cnt + 1) & ~1) * 8u, &bars[st]);
+      }
+    }
+    pj += cnt;
+    if (pj == pn) {
+      if (!pair && pb[1] >= 0) {  // unequal pair: now do the second leaf alone
+        pb[0] = pb[1];
+        pke[0] = pke[1];
+        pcl[0] = pcl[1];
+        pvo[0] = pvo[1];
+        pb[1] = -1;
+        pn = nn[pb[0]];
+        pj = 0;
+      } else {
+        pb[0] = pb[1] = -1;
+      }
+    }
+  };
+
+  if (lane == 0)
+    for (int st = 0; st < NST; ++st) issue(st);
+  __syncwarp();
+  double acc = 0.0;
+  int st = 0;
+  unsigned ph = 0;
+  for (;;) {
+    mbar_wait(&bars[st], ph);
+    const int* d = desc + 8 * st;
+    const int b0 = d[0];
+    if (b0 < 0) break;
+    const int b = half ? d[1] : b0;
+    const int cnt = d[2], flags = d[5];
+    const int ke = half ? d[7] : d[6];
+    const double* dv = sv + static_cast<long long>(st) * STAGE + half * SV + l;
+    const double* dx = sv + static_cast<long long>(st) * STAGE + 2 * SV + half * SX + (half ? d[4] : d[3]);
+    if (b >= 0 && l < ke) {
+      int q = 0;
+      if (flags & 1) {
+        acc = hmul(dv[0], dx[0]);  // t = v_0 x_0 (aca.cpp:613)
+        q = 1;
+      }
+      for (; q + 16 <= cnt; q += 16) {
+        double vv[16], xx[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          vv[u] = dv[(q + u) * KM];
+          xx[u] = dx[q + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) acc = hadd(acc, hmul(vv[u], xx[u]));
+      }
+      for (; q < cnt; ++q) acc = hadd(acc, hmul(dv[q * KM], dx[q]));
+    }
+    if ((flags & 2) && b >= 0) t[static_cast<long long>(b) * KM + l] = l < ke ? acc : 0.0;
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(st);
+    }
+    __syncwarp();
+    if (++st == NST) {
+      st = 0;
+      ph ^= 1u;
+    }
+  }
+}
+
+template <int CH, int NST, int WARPS>
+void launch_pair(HMatrix& h, long long njobs, long long v_base, int max_ctas, cudaStream_t s) {
+  constexpr int STAGE = 2 * CH * 16 + 2 * (CH + 2);
+  const size_t smem = static_cast<size_t>(WARPS) * NST * (8 + 32) + sizeof(double) * WARPS * NST * STAGE;
+  HM_CUDA(cudaFuncSetAttribute(t_pair_kernel<CH, NST, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+  const unsigned grid = static_cast<unsigned>(std::min<long long>((njobs / 2 + WARPS) / WARPS, max_ctas));
+  HM_CUDA(cudaMemsetAsync(h.counter.get(), 0, sizeof(int), s));
+  t_pair_kernel<CH, NST, WARPS><<<grid, WARPS * 32, smem, s>>>(h.aca_order.get(), njobs, h.aca.cl.get(),
+                                                              h.aca.n.get(), h.k_eff.get(), h.v_off.get(), v_base,
+                                                              h.V.get(), h.xm.get(), h.counter.get(), h.t.get());
+  HM_LAUNCH_CHECK();
+}
+
+template <int CH, int NST, int WARPS, bool DYN>
+void launch_fold(HMatrix& h, const int* order, long long njobs, long long v_base, int max_ctas, cudaStream_t s) {
+  const int kmax = static_cast<int>(h.cfg.k);
+  const size_t smem = static_cast<size_t>(WARPS) * NST * (8 + 16) +
+                      sizeof(double) * WARPS * NST * (static_cast<size_t>(CH) * kmax + CH + 2);
+  HM_CUDA(cudaFuncSetAttribute(t_fold_kernel<CH, NST, WARPS, DYN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+  const unsigned grid = static_cast<unsigned>(std::min<long long>((njobs + WARPS - 1) / WARPS, max_ctas));
+  if (DYN) HM_CUDA(cudaMemsetAsync(h.counter.get(), 0, sizeof(int), s));
+  t_fold_kernel<CH, NST, WARPS, DYN><<<grid, WARPS * 32, smem, s>>>(order, njobs, h.aca.cl.get(), h.aca.n.get(),
+                                                              h.k_eff.get(), h.v_off.get(), v_base, h.V.get(),
+                                                              h.xm.get(), kmax, h.counter.get(), h.t.get());
+  HM_LAUNCH_CHECK();
 }
 
 void launch_t(HMatrix& h, long long njobs, long long v_base, cudaStream_t s) {
   if (njobs <= 0) return;
+  const int kmax = static_cast<int>(h.cfg.k);
+  if (kmax > 32) raise(kEinval, "k > 32 not supported by the low-rank apply");
+  if (kmax % 2 == 0) {
+    int sms = 0;
+    HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h.device));
+    if (kmax == 16) {
+      // pairs of leaves per warp, 8 warps x 3 stages x 17 KB per CTA -> 1 CTA (8 warps) per SM
+      launch_pair<32, 3, 4>(h, njobs, v_base, sms * 2, s);
+      return;
+    }
+    if (kmax <= 16) launch_fold<32, 3, 8, true>(h, h.aca_order.get(), njobs, v_base, sms * 2, s);
+    else launch_fold<16, 3, 8, true>(h, h.aca_order.get(), njobs, v_base, sms * 2, s);
+    return;
+  }
+  // odd k: thread-per-(leaf, rank) fallback
   int G = 1;
-  while (G < h.cfg.k) G <<= 1;
-  if (G > 32) raise(kEinval, "k > 32 not supported by the low-rank apply");
-  const long long threads = njobs * G;
-  lowrank_t_kernel<<<grid_for(threads, 256), 256, 0, s>>>(h.aca_order.get(), njobs, h.aca.cl.get(), h.aca.n.get(),
-                                                          h.k_eff.get(), h.v_off.get(), v_base, h.V.get(),
-                                                          h.xm.get(), static_cast<int>(h.cfg.k), G, h.t.get());
+  while (G < kmax) G <<= 1;
+  lowrank_t_kernel<<<grid_for(njobs * G, 256), 256, 0, s>>>(h.aca_order.get(), njobs, h.aca.cl.get(), h.aca.n.get(),
+                                                            h.k_eff.get(), h.v_off.get(), v_base, h.V.get(),
+                                                            h.xm.get(), kmax, G, h.t.get());
   HM_LAUNCH_CHECK();
 }
 
@@ -376,6 +910,19 @@ void plan_far_field(HMatrix& h, cudaStream_t s) {
   h.t.alloc(std::max(h.aca.count * kmax, 1ll), s);
   long long lo, hi;
   own_range(h.aca, h.row_begin, h.row_end, lo, hi);
+  {
+    const int D = h.dmax_leaf;
+    const long long S = h.n >> D;
+    const bool pow2 = S > 0 && (S & (S - 1)) == 0;
+    h.tma_rows = h.cfg.precompute_aca && h.cfg.near_stored && (h.n % (1ll << D)) == 0 && pow2 && S >= 32 &&
+                 S <= 64 && (kmax % 2) == 0 && std::getenv("HM_NO_TMA") == nullptr;
+    h.u_tile_shift = -1;
+    if (h.tma_rows) {
+      int sh = 0;
+      while ((1ll << sh) < S) ++sh;
+      h.u_tile_shift = sh;
+    }
+  }
   if (h.cfg.precompute_aca) {
     h.U.alloc(std::max(uo[hi] - uo[lo], 1ll), s);
     h.V.alloc(std::max(vo[hi] - vo[lo], 1ll), s);
@@ -420,7 +967,21 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
     a.a_lo = alo;
     a.a_hi = ahi;
     h.clk.start(kKRows, s);
-    dispatch_rows(h, a, near, true, s);
+    if (h.tma_rows) {
+      TmaArgs A;
+      A.r = a;
+      A.D = h.dmax_leaf;
+      A.a_tslot = h.aca.tau_slot.get();
+      const long long S = h.n >> h.dmax_leaf;
+      const unsigned ncl = static_cast<unsigned>((h.row_end - h.row_begin) / S);
+      if (S == 64 && h.cfg.k <= 16) rows_tma_kernel<64, 16, 5><<<ncl, 64, 0, s>>>(A);
+      else if (S == 64) rows_tma_kernel<64, 32, 2><<<ncl, 64, 0, s>>>(A);
+      else if (h.cfg.k <= 16) rows_tma_kernel<32, 16, 8><<<ncl, 32, 0, s>>>(A);
+      else rows_tma_kernel<32, 32, 5><<<ncl, 32, 0, s>>>(A);
+      HM_LAUNCH_CHECK();
+    } else {
+      dispatch_rows(h, a, near, true, s);
+    }
     h.clk.stop(kKRows, s);
     return;
   }

@@ -314,6 +314,84 @@ __global__ void runs_kernel(long long cnt, const int* __restrict__ ts, int* __re
   }
 }
 
+// Spans of the canonical chain of deepest cluster c: groups of equal row.lower
+// ascending, inside a group the deeper cluster first (smaller row.upper).
+// mode 0: count, mode 1: fill.
+__global__ void chain_spans_kernel(int D, long long ncl, const long long* __restrict__ slot_lo,
+                                   const int* __restrict__ rs, const int* __restrict__ re, int* __restrict__ cnt,
+                                   const int* __restrict__ ptr, int* __restrict__ spans, int mode) {
+  for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < ncl;
+       c += static_cast<long long>(gridDim.x) * blockDim.x) {
+    int k = 0;
+    int o = mode ? ptr[c] : 0;
+    for (int e0 = 0; e0 <= D;) {
+      const long long lo0 = slot_lo[((1ll << e0) - 1) + (c >> (D - e0))];
+      int e1 = e0;
+      while (e1 + 1 <= D && slot_lo[((1ll << (e1 + 1)) - 1) + (c >> (D - e1 - 1))] == lo0) ++e1;
+      for (int e = e1; e >= e0; --e) {
+        const long long s = ((1ll << e) - 1) + (c >> (D - e));
+        if (rs[s] < 0) continue;
+        if (mode) {
+          spans[2 * (o + k)] = rs[s];
+          spans[2 * (o + k) + 1] = re[s];
+        }
+        ++k;
+      }
+      e0 = e1 + 1;
+    }
+    if (!mode) cnt[c] = k;
+  }
+}
+
+// Morton row -> index of its cluster at depth D
+__global__ void row_cluster_kernel(int D, long long n, const long long* __restrict__ slot_lo,
+                                   const long long* __restrict__ slot_hi, int* __restrict__ rc) {
+  const long long first = (1ll << D) - 1;
+  for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < (1ll << D);
+       c += static_cast<long long>(gridDim.x) * blockDim.x) {
+    for (long long i = slot_lo[first + c]; i < slot_hi[first + c]; ++i) rc[i] = static_cast<int>(c);
+  }
+  (void)n;
+}
+
+void build_spans(HMatrix& h, cudaStream_t s) {
+  const int D = h.dmax_leaf;
+  const long long ncl = 1ll << D;
+  h.row_cluster.alloc(h.n, s);
+  row_cluster_kernel<<<grid_for(ncl, 128, 1 << 16), 128, 0, s>>>(D, h.n, h.slot_lo.get(), h.slot_hi.get(),
+                                                                 h.row_cluster.get());
+  HM_LAUNCH_CHECK();
+  struct Side {
+    LeafList* l;
+    DevBuf<int>* ptr;
+    DevBuf<int>* spans;
+  } sides[2] = {{&h.dense, &h.dspan_ptr, &h.dspans}, {&h.aca, &h.aspan_ptr, &h.aspans}};
+  for (const Side& sd : sides) {
+    DevBuf<int> cnt;
+    cnt.alloc(ncl, s);
+    chain_spans_kernel<<<grid_for(ncl, 128, 1 << 16), 128, 0, s>>>(D, ncl, h.slot_lo.get(), sd.l->run_start.get(),
+                                                                   sd.l->run_end.get(), cnt.get(), nullptr, nullptr,
+                                                                   0);
+    HM_LAUNCH_CHECK();
+    DevBuf<long long> c64;
+    c64.alloc(ncl + 1, s);
+    // widen + scan (int64 scan primitive)
+    std::vector<int> hc(ncl);
+    HM_CUDA(cudaMemcpyAsync(hc.data(), cnt.get(), sizeof(int) * ncl, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+    std::vector<int> hp(ncl + 1, 0);
+    for (long long c = 0; c < ncl; ++c) hp[c + 1] = hp[c] + hc[c];
+    sd.ptr->alloc(ncl + 1, s);
+    HM_CUDA(cudaMemcpyAsync(sd.ptr->get(), hp.data(), sizeof(int) * (ncl + 1), cudaMemcpyHostToDevice, s));
+    sd.spans->alloc(2 * std::max(hp[ncl], 1), s);
+    chain_spans_kernel<<<grid_for(ncl, 128, 1 << 16), 128, 0, s>>>(D, ncl, h.slot_lo.get(), sd.l->run_start.get(),
+                                                                   sd.l->run_end.get(), nullptr, sd.ptr->get(),
+                                                                   sd.spans->get(), 1);
+    HM_LAUNCH_CHECK();
+    HM_CUDA(cudaStreamSynchronize(s));
+  }
+}
+
 void alloc_list(LeafList& l, long long cnt, long long nslots, cudaStream_t s) {
   l.count = cnt;
   l.rl.alloc(cnt, s);
@@ -519,6 +597,7 @@ void build_hmatrix(HMatrix& h, const double* coords_in) {
     }
   }
   HM_CUDA(cudaStreamSynchronize(s));
+  build_spans(h, s);
   h.tm.tree_ms = ms_since(t1);
 
   // algorithmic sizes
