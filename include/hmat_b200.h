@@ -101,6 +101,11 @@ hm_status hm_mvp_device(hm_handle* h, const double* x_dev, double* z_dev, void* 
 hm_status hm_nccl_unique_id(unsigned char id[128]);
 hm_status hm_attach_nccl(hm_handle* h, const unsigned char id[128]);
 
+/* This rank's slice of the product without the allgather: z_slice (host, Morton order)
+ * receives rows [row_begin, row_end) of hm_get_stats.  Lets world > 1 handles be tested
+ * on one GPU (rank by rank). */
+hm_status hm_mvp_local(hm_handle* h, const double* x, double* z_slice);
+
 /* hmat::cg_solve(HMatrix, kernel, b, SolveConfig) -- solver.hpp:27-28 (host vectors). */
 hm_status hm_cg_solve(hm_handle* h, const double* b, double sigma2, double tol, int64_t max_iter, double* x,
                       int64_t* iterations, double* relative_residual);

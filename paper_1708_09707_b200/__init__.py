@@ -92,6 +92,7 @@ _sig("hm_setup_device", C.c_int, [_p, _i64, _i32, _i32, _d, C.POINTER(_Config), 
 _sig("hm_destroy", None, [_p])
 _sig("hm_mvp", C.c_int, [_p, _p, _p, C.POINTER(_Timings)])
 _sig("hm_mvp_device", C.c_int, [_p, _p, _p, _p])
+_sig("hm_mvp_local", C.c_int, [_p, _p, _p])
 _sig("hm_nccl_unique_id", C.c_int, [_p])
 _sig("hm_attach_nccl", C.c_int, [_p, _p])
 _sig("hm_cg_solve", C.c_int, [_p, _p, _d, _d, _i64, _p, C.POINTER(_i64), C.POINTER(_d)])
@@ -116,7 +117,7 @@ _sig("hm_log_port_device", C.c_int, [_i64, _p, _p])
 
 EXPORTED_SYMBOLS = [
     "hm_last_error", "hm_config_default", "hm_device_count", "hm_setup", "hm_setup_device", "hm_destroy",
-    "hm_mvp", "hm_mvp_device", "hm_nccl_unique_id", "hm_attach_nccl", "hm_cg_solve", "hm_relative_error",
+    "hm_mvp", "hm_mvp_device", "hm_mvp_local", "hm_nccl_unique_id", "hm_attach_nccl", "hm_cg_solve", "hm_relative_error",
     "hm_dense_mvp", "hm_get_stats", "hm_get_timings", "hm_get_points", "hm_get_codes", "hm_get_leaves",
     "hm_get_aca", "hm_morton_codes", "hm_morton_order", "hm_aca_dense", "hm_eval_kernel", "hm_exp_port_host",
     "hm_exp_port_device", "hm_log_port_host", "hm_log_port_device", "hm_profile_begin", "hm_profile_end",
@@ -252,6 +253,14 @@ class HMatrix:
     def mvp_device(self, x_ptr: int, z_ptr: int, stream: int = 0) -> None:
         """Device pointers (original ordering) on a CUDA stream handle (0 = the handle's stream)."""
         _check(_lib.hm_mvp_device(self._h, C.c_void_p(x_ptr), C.c_void_p(z_ptr), C.c_void_p(stream or None)))
+
+    def mvp_local(self, x) -> np.ndarray:
+        """This rank's Morton-ordered row slice of H x, without the allgather."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        st = self.stats()
+        z = np.empty(st["row_end"] - st["row_begin"])
+        _check(_lib.hm_mvp_local(self._h, _ptr(x), _ptr(z)))
+        return z
 
     def dense_mvp(self, x) -> np.ndarray:
         x = np.ascontiguousarray(x, dtype=np.float64)

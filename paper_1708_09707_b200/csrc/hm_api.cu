@@ -1,6 +1,5 @@
 // hm_api.cu -- the C ABI (include/hmat_b200.h): host orchestration in C++,
 // exceptions mapped to hm_status at the boundary.
-#include <nccl.h>
 
 #include <chrono>
 #include <cmath>
@@ -12,6 +11,7 @@
 
 #include "../../include/hmat_b200.h"
 #include "hmatrix.h"
+#include "nccl_shim.h"
 #include "primitives.h"
 
 namespace hmb {
@@ -275,14 +275,15 @@ void product(hm_handle* H, const double* x_dev, double* z_dev, cudaStream_t s) {
     // slices are contiguous and may differ in size by the ceil splits.
     const std::vector<long long>& bounds = H->rank_bounds;
     h.clk.start(kKAllgather, s);
-    if (ncclGroupStart() != ncclSuccess) raise(kEnccl, "ncclGroupStart");
+    const NcclApi& nc = NcclApi::get();
+    if (nc.GroupStart() != ncclSuccess) raise(kEnccl, "ncclGroupStart");
     for (int r = 0; r < h.cfg.world; ++r) {
       double* p = h.zm.get() + bounds[r];
-      if (ncclBroadcast(p, p, static_cast<size_t>(bounds[r + 1] - bounds[r]), ncclDouble, r, H->comm, s) !=
+      if (nc.Broadcast(p, p, static_cast<size_t>(bounds[r + 1] - bounds[r]), ncclDouble, r, H->comm, s) !=
           ncclSuccess)
         raise(kEnccl, "ncclBroadcast of the y slice failed");
     }
-    if (ncclGroupEnd() != ncclSuccess) raise(kEnccl, "ncclGroupEnd");
+    if (nc.GroupEnd() != ncclSuccess) raise(kEnccl, "ncclGroupEnd");
     h.clk.stop(kKAllgather, s);
   }
   h.clk.start(kKScatter, s);
@@ -353,7 +354,7 @@ hm_status hm_setup_device(const double* coords_dev, int64_t n, int32_t d, int32_
 void hm_destroy(hm_handle* H) {
   if (!H) return;
   cudaSetDevice(H->h.device);
-  if (H->comm) ncclCommDestroy(H->comm);
+  if (H->comm) NcclApi::get().CommDestroy(H->comm);
   cudaStream_t s = H->h.stream, aux = H->h.aux;
   cudaEvent_t e0 = H->h.ev_fork, e1 = H->h.ev_join;
   cudaStreamSynchronize(s);
@@ -397,10 +398,28 @@ hm_status hm_mvp_device(hm_handle* H, const double* x_dev, double* z_dev, void* 
   });
 }
 
+hm_status hm_mvp_local(hm_handle* H, const double* x, double* z_slice) {
+  return guarded([&] {
+    if (!H || !x || !z_slice) raise(kEinval, "mvp_local: null argument");
+    std::lock_guard<std::mutex> lock(H->mu);
+    HMatrix& h = H->h;
+    HM_CUDA(cudaSetDevice(h.device));
+    cudaStream_t s = h.stream;
+    if (h.xin.size() < static_cast<size_t>(h.n)) h.xin.alloc(h.n, s);
+    HM_CUDA(cudaMemcpyAsync(h.xin.get(), x, sizeof(double) * h.n, cudaMemcpyHostToDevice, s));
+    gather_kernel<<<grid_for(h.n, 256, 1 << 16), 256, 0, s>>>(h.xin.get(), h.perm.get(), h.n, h.xm.get());
+    HM_LAUNCH_CHECK();
+    mvp_morton(h, s);
+    HM_CUDA(cudaMemcpyAsync(z_slice, h.zm.get() + h.row_begin, sizeof(double) * (h.row_end - h.row_begin),
+                            cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 hm_status hm_nccl_unique_id(unsigned char id[128]) {
   return guarded([&] {
     ncclUniqueId u;
-    if (ncclGetUniqueId(&u) != ncclSuccess) raise(kEnccl, "ncclGetUniqueId failed");
+    if (NcclApi::get().GetUniqueId(&u) != ncclSuccess) raise(kEnccl, "ncclGetUniqueId failed");
     static_assert(sizeof(u) == 128, "ncclUniqueId size");
     std::memcpy(id, &u, 128);
   });
@@ -412,7 +431,7 @@ hm_status hm_attach_nccl(hm_handle* H, const unsigned char id[128]) {
     std::memcpy(&u, id, 128);
     HMatrix& h = H->h;
     HM_CUDA(cudaSetDevice(h.device));
-    if (ncclCommInitRank(&H->comm, h.cfg.world, u, h.cfg.rank) != ncclSuccess)
+    if (NcclApi::get().CommInitRank(&H->comm, h.cfg.world, u, h.cfg.rank) != ncclSuccess)
       raise(kEnccl, "ncclCommInitRank failed");
     int g = 0;
     while ((1 << g) < h.cfg.world) ++g;

@@ -1,0 +1,102 @@
+"""Live cross-check of the C restatement against the unmodified reference (oracle/_ref),
+on randomised configurations, plus the SURVEY.md findings the parity targets rest on.
+Skipped where oracle/_ref is not built."""
+import numpy as np
+import pytest
+
+from paper_1708_09707_b200.inputs import axis_major_points, symmetric, uniform_points
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint64)
+
+
+CONFIGS = [
+    # n, d, c_leaf, kernel, k, eta
+    (50, 2, 8, 0, 4, 1.5),
+    (333, 3, 20, 1, 6, 1.2),
+    (1111, 2, 37, 0, 12, 2.0),
+    (2500, 1, 64, 1, 16, 0.8),
+    (4000, 5, 100, 0, 8, 1.5),
+    (1024, 2, 1, 0, 3, 1.5),
+    (700, 4, 700, 0, 16, 1.5),   # N <= C_leaf: one dense leaf
+]
+
+
+@pytest.mark.parametrize("cfg", CONFIGS, ids=[str(c) for c in CONFIGS])
+def test_oracle_equals_reference(oracle, reference, cfg):
+    n, d, c_leaf, kern, k, eta = cfg
+    P = uniform_points(n, d, 1234 + n)
+    ho = oracle.setup(P, kernel=kern, c_leaf=c_leaf, k=k, eta=eta)
+    hr = reference.setup(P, kernel=kern, c_leaf=c_leaf, k=k, eta=eta)
+    co, po = ho.points()
+    cr, pr = hr.points()
+    assert np.array_equal(po, pr) and np.array_equal(bits(co), bits(cr))
+    for w in (0, 1):
+        lo, lr = ho.leaves(w), hr.leaves(w)
+        assert np.array_equal(lo.rows, lr.rows)
+        assert np.array_equal(bits(lo.boxes), bits(lr.boxes))
+    fo, fr = ho.aca_all(), hr.aca_all()
+    assert np.array_equal(fo["k_eff"], fr["k_eff"])
+    assert np.array_equal(fo["row_piv"], fr["row_piv"])
+    for a, b in zip(fo["u"], fr["u"]):
+        assert np.array_equal(bits(a), bits(b))
+    x = symmetric(99, n)
+    assert np.array_equal(bits(ho.mvp(x)), bits(hr.mvp(x)))
+
+
+def test_morton_codes_random(oracle, reference):
+    for d in (1, 2, 3, 5, 7, 20):
+        c = axis_major_points(400, d, 7 + d)
+        assert np.array_equal(oracle.morton_codes(c), reference.morton_codes(c))
+
+
+def test_row_sampled_product_equals_full(oracle, reference):
+    """the row-sampled reconstruction equals mvp() bitwise."""
+    n = 1 << 13
+    P = uniform_points(n, 2, 42)
+    hr = reference.setup(P, c_leaf=64, k=16)
+    ho = oracle.setup(P, c_leaf=64, k=16)
+    x = symmetric(7, n)
+    _, perm = hr.points()
+    z = hr.mvp(x)
+    zm = np.empty(n)
+    zm[np.arange(n)] = z[perm]
+    ranges = [(0, 64), (1024, 1088), (5000, 5100), (8128, 8192)]
+    zr = reference.setup(P, c_leaf=64, k=16).mvp_rows(x, ranges)
+    zo = ho.mvp_rows(x, ranges)
+    for lo, hi in ranges:
+        assert np.array_equal(bits(zr[lo:hi]), bits(zm[lo:hi]))
+        assert np.array_equal(bits(zo[lo:hi]), bits(zm[lo:hi]))
+
+
+def test_f2_single_differs_from_batched(reference):
+    """aca_single stops early on a sub-threshold column, aca_batched keeps
+    scanning; the parity target is the batched semantics (what mvp() uses)."""
+    n = 1 << 12
+    P = uniform_points(n, 2, 42)
+    h = reference.setup(P, c_leaf=64, k=16)
+    lv = h.leaves(1, boxes=False).rows
+    coords, _ = h.points()
+    # materialise a handful of small admissible blocks
+    blocks = []
+    for (rl, ru, cl, cu) in lv[:40]:
+        if ru - rl > 128:
+            continue
+        yi = coords[:, rl:ru]
+        yj = coords[:, cl:cu]
+        r2 = ((yi[:, :, None] - yj[:, None, :]) ** 2).sum(axis=0)
+        blocks.append(np.exp(-r2))
+    kb, _, _, _, _ = reference.aca_dense(blocks, 16, single=False)
+    ks, _, _, _, _ = reference.aca_dense(blocks, 16, single=True)
+    assert np.all(kb >= ks)
+
+
+def test_f3_epsilon_inert_when_eta_above_one(oracle):
+    """the eps criterion uses the admissibility eta; (1-eta) < 0 makes it inert."""
+    n = 1 << 12
+    P = uniform_points(n, 2, 42)
+    x = symmetric(7, n)
+    a = oracle.setup(P, c_leaf=64, k=16, epsilon=1e-6).mvp(x)
+    b = oracle.setup(P, c_leaf=64, k=16).mvp(x)
+    assert np.array_equal(bits(a), bits(b))
