@@ -162,7 +162,7 @@ def run_reference(args):
         if not available("ref"):
             print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libhmat_ref.so was not built"}))
             return
-        r = reference_sample(args, max(1, args.steps // 10), 1 if args.warmup else 0, args.cpu_workers)
+        r = reference_sample(args, max(1, args.steps), 1 if args.warmup else 0, args.cpu_workers)
     except Exception as e:  # noqa: BLE001
         print(json.dumps({"impl": "reference", "unavailable": f"reference run failed: {e}"[:300]}))
         return
@@ -277,6 +277,16 @@ def run_ours(args):
     rows_bytes = 8.0 * (st["S_d_own"] + st["S_lm"] + (st["row_end"] - st["row_begin"]))
     hbm_peak, peak_kind = peaks()
     rows_gbs = rows_bytes / (rows_avg * 1e-3) / 1e9 if rows_avg > 0 else None
+    traffic = None  # dram bytes per launch of the dominant kernel, from the committed ncu capture
+    try:
+        with open(os.path.join(REPO, "profiles", "traffic_c2.json")) as f:
+            tr = json.load(f)
+        c = tr["config"]
+        if (c["n"], c["d"], c["c_leaf"], c["k"], c["mode"]) == (n, d, args.c_leaf, args.k, args.mode) and world == 1:
+            kk = next(v for k, v in tr["kernels"].items() if k.startswith("rows"))
+            traffic = kk["dram_read_bytes"] + kk["dram_write_bytes"]
+    except Exception:  # noqa: BLE001
+        traffic = None
     launches_per_step = sum(c for (_, c) in prof.values()) / prof_steps
 
     # end to end through the C ABI with host buffers (H2D + D2H inside)
@@ -327,9 +337,9 @@ def run_ours(args):
             "work": {"S_d": S_d, "S_l": S_l, "S_lm": S_lm, "S_ln": S_ln, "flops_per_step": flops,
                      "alg_bytes_per_step": alg_bytes, "n_dense": st["n_dense"], "n_aca": st["n_aca"],
                      "aca_rejections": st["aca_rejections"]},
-            "roofline": {"bound": "hbm", "kernel": "rows_kernel (near+far row gather)",
+            "roofline": {"bound": "hbm", "kernel": "rows_tma_kernel (near + far row-cluster product, TMA ring)",
                          "achieved": rows_gbs, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": (rows_gbs / hbm_peak) if rows_gbs else None, "traffic": None,
+                         "frac": (rows_gbs / hbm_peak) if rows_gbs else None, "traffic": traffic,
                          "peak_kind": peak_kind, "alg_bytes_per_launch": rows_bytes, "avg_ms": rows_avg},
             "kernels_ms_per_step": {k: v[0] / max(v[1], 1) * (v[1] / prof_steps) for k, v in prof.items()},
             "cpu_baseline": cpu,
