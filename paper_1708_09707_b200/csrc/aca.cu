@@ -23,21 +23,64 @@
 // order-sensitive quantity, norm2, is summed in parallel with a rigorous error
 // bound; decisions inside the bound fall back to the reference's sequential fold.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "hmatrix.h"
 #include "primitives.h"
+#include "aca_chain.cuh"
 
 namespace hmb {
 
 namespace {
+
+// HM_TRACE=1: per-phase device times of the factorisation on stderr (development aid)
+struct PhaseTrace {
+  bool on = std::getenv("HM_TRACE") != nullptr;
+  cudaEvent_t e[16];
+  const char* name[16];
+  int k = 0;
+  void mark(const char* nm, cudaStream_t s) {
+    if (!on || k >= 16) return;
+    cudaEventCreate(&e[k]);
+    cudaEventRecord(e[k], s);
+    name[k++] = nm;
+  }
+  void dump() {
+    if (!on || k == 0) return;
+    cudaEventSynchronize(e[k - 1]);
+    for (int i = 1; i < k; ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e[i - 1], e[i]);
+      std::fprintf(stderr, "[hm_trace] %-24s %9.3f ms\n", name[i], ms);
+    }
+    for (int i = 0; i < k; ++i) cudaEventDestroy(e[i]);
+    k = 0;
+  }
+};
 
 constexpr int kAcaThreads = 256;
 constexpr int kKmax = 64;        // compile-time cap on the rank
 constexpr int kColBuf = 2048;    // doubles of shared column buffer
 
 // entry sources ---------------------------------------------------------------
-template <int DIM>
+// KIND: -1 runtime kernel kind, 0 Gaussian, 1 Matern (compile-time specialisation
+// keeps the Bessel code out of the Gaussian kernels' registers).
+template <int KIND>
+__device__ __forceinline__ double phi_kind(const KernelParams& kp, double r2) {
+  if constexpr (KIND == 0) return glibc_exp(-r2);
+  else if constexpr (KIND == 1) {
+    if (r2 == 0.0) return kp.matern_norm;
+    const double r = hm_sqrt(r2);
+    return hmul(hmul(bessel_k1(r), r), kp.matern_norm);
+  } else {
+    return phi_r2(kp, r2);
+  }
+}
+
+template <int DIM, int KIND = -1>
 struct KernelEntry {
   const double* coords;
   long long n;
@@ -67,7 +110,7 @@ struct KernelEntry {
         r2 = hadd(r2, hmul(dx, dx));
       }
     }
-    return phi_r2(kp, r2);
+    return phi_kind<KIND>(kp, r2);
   }
 };
 
@@ -92,6 +135,7 @@ struct AcaJob {
   double eps_factor;        // eps (1 - eta) / (1 + eps), aca.cpp:49
   int* counter;
   unsigned long long* rejections;
+  unsigned long long* evals;  // optional (HM_TRACE): [0] column-scan entries, [1] pivot-row entries, [2] blocks
   int tile_shift;           // -1: U rank-major; else log2(S), U row-tiled by S rows
   // explicit-matrix seam: block b entries at dense + dense_off[b], row-major m x n
   const double* dense;
@@ -344,6 +388,721 @@ void launch_kernel_aca(const AcaJob& J, const HMatrix& h, cudaStream_t s) {
   HM_LAUNCH_CHECK();
 }
 
+// ---------------------------------------------------------------------------
+// Team kernel: the same per-block semantics with the block's residual columns in
+// REGISTERS.  A team of NW warps owns one block (m, n <= 64*NW); thread t of the
+// team owns rows t and t + 32*NW, and keeps u_l of its rows in registers (u[l][q]).
+// v_l is kept in shared memory rank-major (s_v[l][j]) so the column scan reads it
+// as a broadcast.  Candidate columns are evaluated W at a time (speculatively):
+// the lowest qualifying one is accepted, the ones before it are consumed, and the
+// ones after it stay cached in registers and receive the single update
+// u_r * v_r[c] of the accepted cross -- the same chain of mul-then-sub steps the
+// reference applies to a freshly evaluated column (aca.cpp:363-364), so the bits
+// are identical while no evaluated entry is wasted.  Reductions are warp
+// butterflies (every lane ends with the same value), combined across the NW warps
+// in warp order through shared memory.
+template <int NW>
+__device__ __forceinline__ void team_sync(int team) {
+  if constexpr (NW == 1) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(NW * 32) : "memory");
+  }
+}
+
+// shared doubles per team: s_v (KC x 64NW), s_col (64NW), s_up (KC), 3 x NW*W partials, misc
+template <int NW, int KC, int W>
+__host__ __device__ constexpr size_t team_stride() {
+  return static_cast<size_t>(KC) * NW * 64 + NW * 64 + KC + 3 * NW * W + 4;
+}
+
+template <int DIM, int KIND, int NW, int KC, int W>
+__global__ void __launch_bounds__(256) aca_team_kernel(AcaJob J, KernelEntry<DIM, KIND> E, int teams_per_cta) {
+  constexpr int RPL = 2;
+  constexpr int TT = NW * 32;   // threads per team
+  constexpr int NCAP = TT * RPL;
+  constexpr int YD = DIM > 0 ? DIM : 1;
+  extern __shared__ double smem[];
+  const int team = threadIdx.x / TT, t = threadIdx.x % TT, lane = t & 31, wib = t >> 5;
+  if (team >= teams_per_cta) return;
+  constexpr int kRed = NW * W;  // per-warp partials
+  double* base = smem + static_cast<size_t>(team) * team_stride<NW, KC, W>();
+  double* s_v = base;                   // KC x NCAP, rank-major
+  double* s_col = s_v + KC * NCAP;      // NCAP (exact folds)
+  double* s_up = s_col + NCAP;          // KC: u_l[p] of the pivot row
+  double* s_rsum = s_up + KC;           // kRed partial sums
+  double* s_rbv = s_rsum + kRed;        // kRed partial maxima
+  int* s_rbi = reinterpret_cast<int*>(s_rbv + kRed);  // kRed ints
+  double* s_misc = s_rbv + kRed + (kRed + 1) / 2;      // [0] pivot value, [1] job, [2] scale, [3] flags
+  const double kEps0sq = 1e-14 * 1e-14;
+  const int kmax = J.kmax;
+
+  for (;;) {
+    if (t == 0) s_misc[1] = static_cast<double>(atomicAdd(J.counter, 1));
+    team_sync<NW>(team);
+    const long long job = static_cast<long long>(s_misc[1]);
+    team_sync<NW>(team);
+    if (job >= J.njobs) return;
+    const int b = J.order[job];
+    const int rl = J.rl[b], m = J.m[b], cl = J.cl[b], n = J.nn[b];
+    double* U = J.U + (J.u_off[b] - J.u_base);
+    double* V = J.V + (J.v_off[b] - J.v_base);
+    const int tsh = J.tile_shift;
+    auto uix = [&](int l, int i) -> long long {
+      if (tsh < 0) return static_cast<long long>(l) * m + i;
+      return ((static_cast<long long>(i >> tsh) * kmax + l) << tsh) + (i & ((1 << tsh) - 1));
+    };
+
+    double y[RPL][YD];
+    bool rv[RPL];
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      const int i = t + q * TT;
+      rv[q] = i < m;
+      if constexpr (DIM > 0) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) y[q][a] = rv[q] ? __ldg(E.coords + a * E.n + rl + i) : 0.0;
+      }
+    }
+    auto entry = [&](int q, long long colpt) -> double {
+      if constexpr (DIM > 0) {
+        return E.eval(y[q], colpt);
+      } else {
+        double yy[20];
+        E.load(rl + t + q * TT, yy);
+        return E.eval(yy, colpt);
+      }
+    };
+
+    // u_l of the own rows, right-aligned: at rank r, u_l lives in uR[q][KC - r + l]
+    double uR[RPL][KC];
+#pragma unroll
+    for (int q = 0; q < RPL; ++q)
+#pragma unroll
+      for (int j = 0; j < KC; ++j) uR[q][j] = 0.0;
+    double res[W][RPL];
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) res[w][q] = 0.0;
+    unsigned used = 0;  // RPL bits: own rows that are pivots
+    int next = 0, cached = 0, k_eff = 0;
+    unsigned long long rejections = 0, ev_col = 0, ev_row = 0;
+    double scale = -1.0;
+    const double gm = static_cast<double>(m) * 1.2e-16;
+
+    for (int r = 0; r < kmax; ++r) {
+      int acc_w = -1;
+      double acc[RPL];
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) acc[q] = 0.0;
+      const double* vb = s_v + static_cast<long long>(r - KC) * NCAP;  // chain base (see aca_chain.cuh)
+      while (next < n) {
+        const int wcols = min(W, n - next);
+        ev_col += static_cast<unsigned long long>(wcols - cached) * m;
+        // fresh evaluations of window columns [cached, wcols): entry, then the chain
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          if (w >= cached && w < wcols) {
+            const int c = next + w;
+#pragma unroll
+            for (int q = 0; q < RPL; ++q)
+              res[w][q] = rv[q] ? Chain<KC>::run(entry(q, cl + c), uR[q], r, vb + c, NCAP) : 0.0;
+          }
+        }
+        // qualification of every window column: norm2 (parallel, bounded) and "some
+        // unused row is non-zero" (best > 0, aca.cpp:381)
+        double sum[W];
+        unsigned nzmask = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          sum[w] = 0.0;
+          bool nz = false;
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) {
+            if (rv[q]) {
+              const double a = res[w][q];
+              sum[w] = hadd(sum[w], hmul(a, a));
+              nz |= !((used >> q) & 1u) && fabs(a) > 0.0;
+            }
+          }
+#pragma unroll
+          for (int o = 16; o; o >>= 1) sum[w] = hadd(sum[w], __shfl_xor_sync(0xffffffffu, sum[w], o));
+          if (__any_sync(0xffffffffu, nz)) nzmask |= 1u << w;
+        }
+        if constexpr (NW > 1) {
+          if (lane == 0) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) s_rsum[wib * W + w] = sum[w];
+            s_rbi[wib] = static_cast<int>(nzmask);
+          }
+          team_sync<NW>(team);
+          nzmask = 0;
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            sum[w] = s_rsum[w];
+            for (int g = 1; g < NW; ++g) sum[w] = hadd(sum[w], s_rsum[g * W + w]);
+          }
+          for (int g = 0; g < NW; ++g) nzmask |= static_cast<unsigned>(s_rbi[g]);
+          team_sync<NW>(team);
+        }
+        // decision: lowest qualifying column of the window (uniform across the team)
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          if (acc_w < 0 && w < wcols && ((nzmask >> w) & 1u)) {
+            bool qf = false;
+            if (scale < 0.0) {
+              qf = true;
+            } else {
+              const double T = hmul(kEps0sq, scale);
+              const double lo = hmul(sum[w], 1.0 - 4.0 * gm), hi = hmul(sum[w], 1.0 + 4.0 * gm);
+              if (lo > T) {
+                qf = true;
+              } else if (hi <= T) {
+                qf = false;
+              } else {  // ambiguous: the reference's sequential left fold (aca.cpp:373-374)
+#pragma unroll
+                for (int qq = 0; qq < RPL; ++qq)
+                  if (rv[qq]) s_col[t + qq * TT] = res[w][qq];
+                team_sync<NW>(team);
+                double f = hmul(s_col[0], s_col[0]);
+                for (int i = 1; i < m; ++i) f = hadd(f, hmul(s_col[i], s_col[i]));
+                team_sync<NW>(team);
+                qf = f > T;
+              }
+            }
+            if (qf) acc_w = w;
+          }
+        }
+        const int consumed = acc_w >= 0 ? acc_w + 1 : wcols;
+        rejections += static_cast<unsigned long long>(acc_w >= 0 ? acc_w : wcols);
+        if (acc_w >= 0) {
+#pragma unroll
+          for (int w = 0; w < W; ++w)
+            if (w == acc_w)
+#pragma unroll
+              for (int q = 0; q < RPL; ++q) acc[q] = res[w][q];
+        }
+        for (int sh = 0; sh < consumed; ++sh) {
+#pragma unroll
+          for (int w = 0; w + 1 < W; ++w)
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) res[w][q] = res[w + 1][q];
+        }
+        cached = acc_w >= 0 ? wcols - consumed : 0;
+        next += consumed;
+        if (acc_w >= 0) break;
+      }
+      if (acc_w < 0) break;  // no usable column left (aca.cpp:442-443)
+      const int cstar = next - 1;
+
+      // pivot row: argmax |u_hat| over unused rows, first index wins (aca.cpp:367, 375-376)
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        const double av = fabs(acc[q]);
+        if (rv[q] && !((used >> q) & 1u) && av > bv) {
+          bv = av;
+          bi = t + q * TT;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        argmax_combine(bv, bi, ov, oi);
+      }
+      if constexpr (NW > 1) {
+        if (lane == 0) {
+          s_rbv[wib] = bv;
+          s_rbi[wib] = bi;
+        }
+        team_sync<NW>(team);
+        bv = s_rbv[0];
+        bi = s_rbi[0];
+        for (int g = 1; g < NW; ++g) argmax_combine(bv, bi, s_rbv[g], s_rbi[g]);
+      }
+      const int p = bi;
+
+      // (first cross) scale2 = exact left fold of the column (aca.cpp:491)
+      if (r == 0) {
+#pragma unroll
+        for (int q = 0; q < RPL; ++q)
+          if (rv[q]) s_col[t + q * TT] = acc[q];
+        team_sync<NW>(team);
+        if (t == 0) {
+          double f = hmul(s_col[0], s_col[0]);
+          for (int i = 1; i < m; ++i) f = hadd(f, hmul(s_col[i], s_col[i]));
+          s_misc[2] = f;
+        }
+      }
+      const int pt = p % TT, pq = p / TT;
+      if (t == pt) {
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+          if (q == pq) {
+            s_misc[0] = acc[q];
+#pragma unroll
+            for (int j = 0; j < KC; ++j)
+              if (j >= KC - r) s_up[j - (KC - r)] = uR[q][j];
+          }
+        }
+        used |= 1u << pq;
+      }
+      team_sync<NW>(team);
+      if (r == 0) scale = s_misc[2];
+      const double pivot_val = s_misc[0];
+      // u_r = u_hat / pivot (aca.cpp:466-470), appended right-aligned
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+#pragma unroll
+        for (int j = 0; j + 1 < KC; ++j) uR[q][j] = uR[q][j + 1];
+        uR[q][KC - 1] = rv[q] ? __ddiv_rn(acc[q], pivot_val) : 0.0;
+      }
+      // v_r = A(p,:) - sum_l u_l[p] v_l (aca.cpp:474-481)
+      ev_row += n;
+      {
+        double yp[DIM > 0 ? DIM : 20];
+        E.load(rl + p, yp);
+        for (int j = t; j < n; j += TT) {
+          double a = E.eval(yp, cl + j);
+          for (int l = 0; l < r; ++l) a = hsub(a, hmul(s_up[l], s_v[l * NCAP + j]));
+          s_v[r * NCAP + j] = a;
+        }
+      }
+      team_sync<NW>(team);
+      // cached window columns receive this cross (the next step of their chain)
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        if (w < cached) {
+          const double vr = s_v[r * NCAP + next + w];
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) res[w][q] = hsub(res[w][q], hmul(uR[q][KC - 1], vr));
+        }
+      }
+      if (t == 0) {
+        J.row_piv[static_cast<long long>(b) * kmax + r] = p;
+        J.col_piv[static_cast<long long>(b) * kmax + r] = cstar;
+      }
+      k_eff = r + 1;
+    }
+    // factors: U (layout uix), V interleaved n x kmax, zero past k_eff
+#pragma unroll
+    for (int j = 0; j < KC; ++j) {
+      const int l = j - (KC - k_eff);  // u_l at uR[q][KC - k_eff + l]
+      if (l >= 0) {
+#pragma unroll
+        for (int q = 0; q < RPL; ++q)
+          if (rv[q]) U[uix(l, t + q * TT)] = uR[q][j];
+      }
+    }
+    for (int l = k_eff; l < kmax; ++l)
+#pragma unroll
+      for (int q = 0; q < RPL; ++q)
+        if (rv[q]) U[uix(l, t + q * TT)] = 0.0;
+    for (int idx = t; idx < n * kmax; idx += TT) {
+      const int j = idx / kmax, l = idx - j * kmax;
+      V[idx] = l < k_eff ? s_v[l * NCAP + j] : 0.0;
+    }
+    for (int l = k_eff + t; l < kmax; l += TT) {
+      J.row_piv[static_cast<long long>(b) * kmax + l] = -1;
+      J.col_piv[static_cast<long long>(b) * kmax + l] = -1;
+    }
+    if (t == 0) {
+      J.k_eff[b] = k_eff;
+      if (J.rejections && rejections) atomicAdd(J.rejections, rejections);
+      if (J.evals) {
+        atomicAdd(J.evals, ev_col);
+        atomicAdd(J.evals + 1, ev_row);
+        atomicAdd(J.evals + 2, 1ull);
+      }
+    }
+    team_sync<NW>(team);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Window kernel: the team kernel's row-in-register layout with a SHARED-memory
+// window of W candidate columns (ring slots col % W, padded stride).  Columns are
+// evaluated W at a time by all threads of the team (fill), their qualification is
+// decided by G = TT/W threads per column (partial sums + the rigorous bound, the
+// reference's sequential fold when ambiguous), and the unconsumed columns stay in
+// the window, receiving each accepted cross as the next step of their chain.  In
+// the noise-floor regime (most columns rejected) this turns the scan
+// into dense, barrier-amortised evaluation.  v_l lives in shared memory (VSM) or
+// directly in the interleaved V factor.
+template <int NW, int KC, int W, bool VSM>
+__host__ __device__ constexpr size_t win_stride() {
+  return static_cast<size_t>(W) * (NW * 64 + 1) + (VSM ? static_cast<size_t>(KC) * NW * 64 : 0) + KC + 2 * NW + W +
+         NW * 64 / 8 + 8;
+}
+
+template <int DIM, int KIND, int NW, int KC, int W, bool VSM, int MINB>
+__global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
+    aca_win_kernel(AcaJob J, KernelEntry<DIM, KIND> E, int teams_per_cta) {
+  constexpr int RPL = 2;
+  constexpr int TT = NW * 32;
+  constexpr int NCAP = TT * RPL;
+  constexpr int PS = NCAP + 1;  // padded slot stride (bank spread for the per-column folds)
+  constexpr int G = TT / W;     // threads per column in the qualification pass
+  static_assert(TT % W == 0 && G >= 1 && (G <= 32 || G % 32 == 0), "window / team shape");
+  constexpr int GL = G < 32 ? G : 32;  // lanes of one column inside a warp
+  constexpr int YD = DIM > 0 ? DIM : 1;
+  extern __shared__ double smem[];
+  const int team = threadIdx.x / TT, t = threadIdx.x % TT, lane = t & 31, wib = t >> 5;
+  if (team >= teams_per_cta) return;
+  double* base = smem + static_cast<size_t>(team) * win_stride<NW, KC, W, VSM>();
+  double* s_win = base;
+  double* s_v = s_win + W * PS;
+  double* s_up = s_v + (VSM ? KC * NCAP : 0);
+  double* s_rbv = s_up + KC;
+  int* s_rbi = reinterpret_cast<int*>(s_rbv + NW);
+  int* s_state = reinterpret_cast<int*>(s_rbv + 2 * NW);
+  unsigned char* s_used = reinterpret_cast<unsigned char*>(s_rbv + 2 * NW + W);
+  double* s_misc = s_rbv + 2 * NW + W + NCAP / 8;  // [0] job, [1] scale, [2] exact-fold verdict
+  const double kEps0sq = 1e-14 * 1e-14;
+  const int kmax = J.kmax;
+
+  for (;;) {
+    if (t == 0) s_misc[0] = static_cast<double>(atomicAdd(J.counter, 1));
+    for (int i = t; i < NCAP; i += TT) s_used[i] = 0;
+    team_sync<NW>(team);
+    const long long job = static_cast<long long>(s_misc[0]);
+    team_sync<NW>(team);
+    if (job >= J.njobs) return;
+    const int b = J.order[job];
+    const int rl = J.rl[b], m = J.m[b], cl = J.cl[b], n = J.nn[b];
+    double* U = J.U + (J.u_off[b] - J.u_base);
+    double* V = J.V + (J.v_off[b] - J.v_base);
+    const int tsh = J.tile_shift;
+    auto uix = [&](int l, int i) -> long long {
+      if (tsh < 0) return static_cast<long long>(l) * m + i;
+      return ((static_cast<long long>(i >> tsh) * kmax + l) << tsh) + (i & ((1 << tsh) - 1));
+    };
+    auto vat = [&](int l, int j) -> double& {
+      if constexpr (VSM) return s_v[l * NCAP + j];
+      else return V[static_cast<long long>(j) * kmax + l];
+    };
+
+    double y[RPL][YD];
+    bool rv[RPL];
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      const int i = t + q * TT;
+      rv[q] = i < m;
+      if constexpr (DIM > 0) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) y[q][a] = rv[q] ? __ldg(E.coords + a * E.n + rl + i) : 0.0;
+      }
+    }
+    auto entry = [&](int q, long long colpt) -> double {
+      if constexpr (DIM > 0) {
+        return E.eval(y[q], colpt);
+      } else {
+        double yy[20];
+        E.load(rl + t + q * TT, yy);
+        return E.eval(yy, colpt);
+      }
+    };
+    double uR[RPL][KC];  // right-aligned u_l of the own rows (aca_chain.cuh)
+#pragma unroll
+    for (int q = 0; q < RPL; ++q)
+#pragma unroll
+      for (int j = 0; j < KC; ++j) uR[q][j] = 0.0;
+    int next = 0, filled = 0, k_eff = 0;
+    unsigned long long rejections = 0, ev_col = 0, ev_row = 0;
+    double scale = -1.0;
+    const double gm = static_cast<double>(m) * 1.2e-16;
+
+    for (int r = 0; r < kmax; ++r) {
+      int acc_w = -1;
+      while (next < n) {
+        const int wcols = min(W, n - next);
+        ev_col += static_cast<unsigned long long>(wcols - filled) * m;
+        // fill: fresh window columns, entry then the reference chain over l < r
+        for (int co = filled; co < wcols; ++co) {
+          const int col = next + co;
+          double* dst = s_win + (col % W) * PS;
+          const double* vb;
+          int vs;
+          if constexpr (VSM) {
+            vb = s_v + static_cast<long long>(r - KC) * NCAP + col;
+            vs = NCAP;
+          } else {
+            vb = V + static_cast<long long>(col) * kmax + (r - KC);
+            vs = 1;
+          }
+          double a0 = rv[0] ? entry(0, cl + col) : 0.0;
+          double a1 = rv[1] ? entry(1, cl + col) : 0.0;
+          Chain<KC>::run2(a0, a1, uR[0], uR[1], r, vb, vs);
+          if (rv[0]) dst[t] = a0;
+          if (rv[1]) dst[t + TT] = a1;
+        }
+        filled = wcols;
+        team_sync<NW>(team);
+        // qualification: G threads per column; state 0 no, 1 yes, 2 ambiguous
+        {
+          const int w = t / G, g = t % G;
+          double sum = 0.0;
+          int nz = 0;
+          if (w < wcols) {
+            const double* src = s_win + ((next + w) % W) * PS;
+            for (int i = g; i < m; i += G) {
+              const double a = src[i];
+              sum = hadd(sum, hmul(a, a));
+              nz |= (!s_used[i] && fabs(a) > 0.0) ? 1 : 0;
+            }
+          }
+#pragma unroll
+          for (int o = GL / 2; o; o >>= 1) {
+            sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+            nz |= __shfl_xor_sync(0xffffffffu, nz, o);
+          }
+          if constexpr (G > 32) {  // a column spans G/32 warps: combine their partials in warp order
+            if (lane == 0) {
+              s_rbv[wib] = sum;
+              s_rbi[wib] = nz;
+            }
+            team_sync<NW>(team);
+            if (g == 0 && w < wcols) {
+              sum = s_rbv[wib];
+              nz = s_rbi[wib];
+              for (int k2 = 1; k2 < G / 32; ++k2) {
+                sum = hadd(sum, s_rbv[wib + k2]);
+                nz |= s_rbi[wib + k2];
+              }
+            }
+          }
+          if (g == 0 && w < wcols) {
+            int st = 0;
+            if (nz) {
+              if (scale < 0.0) {
+                st = 1;
+              } else {
+                const double T = hmul(kEps0sq, scale);
+                const double lo = hmul(sum, 1.0 - 4.0 * gm), hi = hmul(sum, 1.0 + 4.0 * gm);
+                st = lo > T ? 1 : (hi <= T ? 0 : 2);
+              }
+            }
+            s_state[w] = st;
+          }
+        }
+        team_sync<NW>(team);
+        for (int w = 0; w < wcols; ++w) {
+          int st = s_state[w];
+          if (st == 2) {  // the reference's sequential left fold (aca.cpp:373-374 / 414-415)
+            if (t == 0) {
+              const double* src = s_win + ((next + w) % W) * PS;
+              double f = hmul(src[0], src[0]);
+              for (int i = 1; i < m; ++i) f = hadd(f, hmul(src[i], src[i]));
+              s_misc[2] = f > hmul(kEps0sq, scale) ? 1.0 : 0.0;
+            }
+            team_sync<NW>(team);
+            st = s_misc[2] != 0.0 ? 1 : 0;
+            team_sync<NW>(team);
+          }
+          if (st == 1) {
+            acc_w = w;
+            break;
+          }
+        }
+        const int consumed = acc_w >= 0 ? acc_w + 1 : wcols;
+        rejections += static_cast<unsigned long long>(acc_w >= 0 ? acc_w : wcols);
+        next += consumed;
+        filled = acc_w >= 0 ? wcols - consumed : 0;
+        if (acc_w >= 0) break;
+      }
+      if (acc_w < 0) break;  // no usable column left (aca.cpp:442-443)
+      const int cstar = next - 1;
+      const double* acol = s_win + (cstar % W) * PS;
+
+      // pivot row: argmax |u_hat| over unused rows, first index wins (aca.cpp:367, 375-376)
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        const int i = t + q * TT;
+        if (rv[q] && !s_used[i]) {
+          const double av = fabs(acol[i]);
+          if (av > bv) {
+            bv = av;
+            bi = i;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        argmax_combine(bv, bi, ov, oi);
+      }
+      if constexpr (NW > 1) {
+        if (lane == 0) {
+          s_rbv[wib] = bv;
+          s_rbi[wib] = bi;
+        }
+        team_sync<NW>(team);
+        bv = s_rbv[0];
+        bi = s_rbi[0];
+        for (int g = 1; g < NW; ++g) argmax_combine(bv, bi, s_rbv[g], s_rbi[g]);
+      }
+      const int p = bi;
+      if (r == 0 && t == 0) {  // scale2 = exact left fold of the first accepted column (aca.cpp:491)
+        double f = hmul(acol[0], acol[0]);
+        for (int i = 1; i < m; ++i) f = hadd(f, hmul(acol[i], acol[i]));
+        s_misc[1] = f;
+      }
+      const int pt = p % TT, pq = p / TT;
+      if (t == pt) {
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+          if (q == pq) {
+#pragma unroll
+            for (int j = 0; j < KC; ++j)
+              if (j >= KC - r) s_up[j - (KC - r)] = uR[q][j];
+          }
+        }
+      }
+      team_sync<NW>(team);
+      if (r == 0) scale = s_misc[1];
+      const double pivot_val = acol[p];
+      // u_r = u_hat / pivot (aca.cpp:466-470), appended right-aligned
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        const double nu = rv[q] ? __ddiv_rn(acol[t + q * TT], pivot_val) : 0.0;
+#pragma unroll
+        for (int j = 0; j + 1 < KC; ++j) uR[q][j] = uR[q][j + 1];
+        uR[q][KC - 1] = nu;
+      }
+      // v_r = A(p,:) - sum_l u_l[p] v_l (aca.cpp:474-481); window columns already hold it
+      ev_row += n;
+      {
+        double yp[DIM > 0 ? DIM : 20];
+        E.load(rl + p, yp);
+        for (int j = t; j < n; j += TT) {
+          double a;
+          if (j >= next && j < next + filled) {
+            a = s_win[(j % W) * PS + p];
+          } else {
+            a = E.eval(yp, cl + j);
+            for (int l = 0; l < r; ++l) a = hsub(a, hmul(s_up[l], vat(l, j)));
+          }
+          vat(r, j) = a;
+        }
+      }
+      team_sync<NW>(team);
+      if (t == pt) s_used[p] = 1;  // after every reader of the old flag (argmax above)
+      // window columns receive this cross (next step of their chain)
+      for (int co = 0; co < filled; ++co) {
+        const int col = next + co;
+        const double vr = vat(r, col);
+        double* dst = s_win + (col % W) * PS;
+#pragma unroll
+        for (int q = 0; q < RPL; ++q)
+          if (rv[q]) dst[t + q * TT] = hsub(dst[t + q * TT], hmul(uR[q][KC - 1], vr));
+      }
+      if (t == 0) {
+        J.row_piv[static_cast<long long>(b) * kmax + r] = p;
+        J.col_piv[static_cast<long long>(b) * kmax + r] = cstar;
+      }
+      k_eff = r + 1;
+    }
+    // factors: U (layout uix), V interleaved n x kmax, zero past k_eff
+#pragma unroll
+    for (int j = 0; j < KC; ++j) {
+      const int l = j - (KC - k_eff);
+      if (l >= 0) {
+#pragma unroll
+        for (int q = 0; q < RPL; ++q)
+          if (rv[q]) U[uix(l, t + q * TT)] = uR[q][j];
+      }
+    }
+    for (int l = k_eff; l < kmax; ++l)
+#pragma unroll
+      for (int q = 0; q < RPL; ++q)
+        if (rv[q]) U[uix(l, t + q * TT)] = 0.0;
+    if constexpr (VSM) {
+      team_sync<NW>(team);
+      for (int idx = t; idx < n * kmax; idx += TT) {
+        const int j = idx / kmax, l = idx - j * kmax;
+        V[idx] = l < k_eff ? s_v[l * NCAP + j] : 0.0;
+      }
+    } else {
+      for (int idx = t; idx < n * (kmax - k_eff); idx += TT) {
+        const int j = idx / (kmax - k_eff), l = k_eff + idx % (kmax - k_eff);
+        V[static_cast<long long>(j) * kmax + l] = 0.0;
+      }
+    }
+    for (int l = k_eff + t; l < kmax; l += TT) {
+      J.row_piv[static_cast<long long>(b) * kmax + l] = -1;
+      J.col_piv[static_cast<long long>(b) * kmax + l] = -1;
+    }
+    if (t == 0) {
+      J.k_eff[b] = k_eff;
+      if (J.rejections && rejections) atomicAdd(J.rejections, rejections);
+      if (J.evals) {
+        atomicAdd(J.evals, ev_col);
+        atomicAdd(J.evals + 1, ev_row);
+        atomicAdd(J.evals + 2, 1ull);
+      }
+    }
+    team_sync<NW>(team);
+  }
+}
+
+template <int DIM, int KIND, int NW, int KC, int W, bool VSM, int MINB = 1>
+void launch_win(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, cudaStream_t s) {
+  if (J.njobs <= 0) return;
+  constexpr int teams = NW >= 4 ? 1 : 4 / NW;
+  const size_t smem = teams * win_stride<NW, KC, W, VSM>() * sizeof(double);
+  auto kfn = aca_win_kernel<DIM, KIND, NW, KC, W, VSM, MINB>;
+  HM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int occ = 0;
+  HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, teams * NW * 32, smem));
+  const long long ctas = std::min<long long>((J.njobs + teams - 1) / teams, static_cast<long long>(std::max(occ, 1)) * sms);
+  kfn<<<static_cast<unsigned>(std::max(ctas, 1ll)), teams * NW * 32, smem, s>>>(J, E, teams);
+  HM_LAUNCH_CHECK();
+}
+
+constexpr int kTeamW = 4;  // candidate columns per wave
+
+template <int DIM, int KIND, int NW, int KC>
+void launch_team(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, cudaStream_t s) {
+  if (J.njobs <= 0) return;
+  constexpr int teams = NW >= 4 ? 1 : 4 / NW;
+  const size_t smem = teams * team_stride<NW, KC, kTeamW>() * sizeof(double);
+  auto kfn = aca_team_kernel<DIM, KIND, NW, KC, kTeamW>;
+  HM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int occ = 0;
+  HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, teams * NW * 32, smem));
+  const long long ctas = std::min<long long>((J.njobs + teams - 1) / teams, static_cast<long long>(std::max(occ, 1)) * sms);
+  kfn<<<static_cast<unsigned>(std::max(ctas, 1ll)), teams * NW * 32, smem, s>>>(J, E, teams);
+  HM_LAUNCH_CHECK();
+}
+
+// ACA size classes: team kernels for max(m, n) <= 64 * NW (NW = 1, 2, 4, 8), the
+// CTA kernel for larger blocks, for k > 32 and for the epsilon criterion.
+constexpr int kAcaClasses = 6;
+constexpr int kAcaCta = kAcaClasses - 1;  // the CTA kernel's class
+__host__ __device__ inline int aca_class(int m, int n, long long kmax, bool has_eps) {
+  if (has_eps || kmax > 32) return kAcaCta;
+  const int c = m > n ? m : n;
+  return c <= 64 ? 0 : c <= 128 ? 1 : c <= 256 ? 2 : c <= 512 ? 3 : c <= 1024 ? 4 : kAcaCta;
+}
+
+__global__ void class_key_kernel(const int* __restrict__ m, const int* __restrict__ nn, long long begin, long long cnt,
+                                 int kmax, int has_eps, unsigned long long* __restrict__ keys,
+                                 unsigned* __restrict__ vals) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < cnt;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long b = begin + i;
+    const int cls = aca_class(m[b], nn[b], kmax, has_eps != 0);
+    keys[i] = (static_cast<unsigned long long>(cls) << 32) | static_cast<unsigned long long>(0x7fffffff - nn[b]);
+    vals[i] = static_cast<unsigned>(b);
+  }
+}
+
 __global__ void size_key_kernel(const int* __restrict__ m, const int* __restrict__ nn, long long begin, long long cnt,
                                 unsigned long long* __restrict__ keys, unsigned* __restrict__ vals) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < cnt;
@@ -365,6 +1124,8 @@ void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStrea
   const long long cnt = leaf_end - leaf_begin;
   if (cnt <= 0) return;
   if (h.cfg.k > kKmax) raise(kEinval, "k > 64 is not supported by the device ACA");
+  PhaseTrace tr, tra;
+  tr.mark("start", s);
   // largest-first schedule
   DevBuf<unsigned long long> keys;
   keys.alloc(cnt, s);
@@ -405,13 +1166,117 @@ void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStrea
   J.eps_factor = h.cfg.epsilon * (1.0 - h.cfg.eta) / (1.0 + h.cfg.epsilon);
   J.counter = h.counter.get();
   J.rejections = rej.get();
+  J.evals = nullptr;
   J.tile_shift = h.u_tile_shift;
+  // size classes (team kernels for small blocks, the CTA kernel for the rest)
+  const bool eps = h.cfg.has_epsilon;
+  long long ccount[kAcaClasses] = {};
+  for (long long b = leaf_begin; b < leaf_end; ++b) ++ccount[aca_class(h.aca.h_m[b], h.aca.h_n[b], h.cfg.k, eps)];
+  DevBuf<int> jobs;
+  jobs.alloc(cnt, s);
+  class_key_kernel<<<grid_for(cnt, 256, 1 << 16), 256, 0, s>>>(h.aca.m.get(), h.aca.n.get(), leaf_begin, cnt,
+                                                                static_cast<int>(h.cfg.k), eps ? 1 : 0, keys.get(),
+                                                                reinterpret_cast<unsigned*>(jobs.get()));
+  HM_LAUNCH_CHECK();
+  radix_sort_pairs(keys.get(), reinterpret_cast<unsigned*>(jobs.get()), cnt, s);
+  tr.mark("schedules (2 sorts)", s);
+  DevBuf<int> counters;
+  counters.alloc(kAcaClasses, s);
+  counters.zero(s);
+  int sms = 0;
+  HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h.device));
+  long long first[kAcaClasses + 1];
+  first[0] = 0;
+  for (int c = 0; c < kAcaClasses; ++c) first[c + 1] = first[c] + ccount[c];
+  DevBuf<unsigned long long> evals;
+  if (tr.on) {
+    evals.alloc(3 * kAcaClasses, s);
+    evals.zero(s);
+  }
+  auto sub = [&](int c) {
+    AcaJob Jc = J;
+    Jc.evals = tr.on ? evals.get() + 3 * c : nullptr;
+    Jc.order = jobs.get() + first[c];
+    Jc.njobs = ccount[c];
+    Jc.counter = counters.get() + c;
+    return Jc;
+  };
+  // large blocks on the auxiliary stream, concurrently with the team kernels
+  if (ccount[kAcaCta] > 0) {
+    HM_CUDA(cudaEventRecord(h.ev_fork, s));
+    HM_CUDA(cudaStreamWaitEvent(h.aux, h.ev_fork, 0));
+    const AcaJob Jb = sub(kAcaCta);
+    tra.mark("start", h.aux);
+    switch (h.d) {
+      case 1: launch_kernel_aca<1>(Jb, h, h.aux); break;
+      case 2: launch_kernel_aca<2>(Jb, h, h.aux); break;
+      case 3: launch_kernel_aca<3>(Jb, h, h.aux); break;
+      case 4: launch_kernel_aca<4>(Jb, h, h.aux); break;
+      default: launch_kernel_aca<0>(Jb, h, h.aux); break;
+    }
+    tra.mark("cta kernel (>512, aux)", h.aux);
+  }
+  auto teams_kind = [&](auto dimc, auto kindc) {
+    constexpr int DIM = decltype(dimc)::value;
+    constexpr int KIND = decltype(kindc)::value;
+    KernelEntry<DIM, KIND> E{h.coords.get(), h.n, h.d, h.kp};
+    const bool team = std::getenv("HM_ACA_TEAM") != nullptr;  // A/B: register-window kernels
+    if (h.cfg.k <= 16) {
+      const char* v16 = std::getenv("HM_W16");
+      const char* v8 = std::getenv("HM_W8");
+      if (v16 && v16[0] == '1') launch_win<DIM, KIND, 16, 16, 16, false>(sub(4), E, sms, s);
+      else launch_win<DIM, KIND, 16, 16, 8, true>(sub(4), E, sms, s);
+      tr.mark("win NW=16 (<=1024)", s);
+      if (team) launch_team<DIM, KIND, 8, 16>(sub(3), E, sms, s);
+      else if (v8 && v8[0] == '1') launch_win<DIM, KIND, 8, 16, 16, true>(sub(3), E, sms, s);
+      else if (v8 && v8[0] == '2') launch_win<DIM, KIND, 8, 16, 32, false>(sub(3), E, sms, s);
+      else launch_win<DIM, KIND, 8, 16, 16, false, 2>(sub(3), E, sms, s);
+      tr.mark("NW=8 (<=512)", s);
+      if (team) launch_team<DIM, KIND, 4, 16>(sub(2), E, sms, s);
+      else launch_win<DIM, KIND, 4, 16, 32, true>(sub(2), E, sms, s);
+      tr.mark("NW=4 (<=256)", s);
+      if (team) launch_team<DIM, KIND, 2, 16>(sub(1), E, sms, s);
+      else launch_win<DIM, KIND, 2, 16, 16, true>(sub(1), E, sms, s);
+      tr.mark("NW=2 (<=128)", s);
+      if (team) launch_team<DIM, KIND, 1, 16>(sub(0), E, sms, s);
+      else launch_win<DIM, KIND, 1, 16, 16, true>(sub(0), E, sms, s);
+      tr.mark("NW=1 (<=64)", s);
+    } else {
+      launch_win<DIM, KIND, 16, 32, 16, false>(sub(4), E, sms, s);
+      launch_win<DIM, KIND, 8, 32, 32, false>(sub(3), E, sms, s);
+      launch_win<DIM, KIND, 4, 32, 32, false>(sub(2), E, sms, s);
+      launch_win<DIM, KIND, 2, 32, 16, true>(sub(1), E, sms, s);
+      launch_win<DIM, KIND, 1, 32, 16, true>(sub(0), E, sms, s);
+    }
+  };
+  auto teams_for = [&](auto dimc) {
+    if (h.kp.kind == kGaussian) teams_kind(dimc, std::integral_constant<int, 0>{});
+    else teams_kind(dimc, std::integral_constant<int, 1>{});
+  };
   switch (h.d) {
-    case 1: launch_kernel_aca<1>(J, h, s); break;
-    case 2: launch_kernel_aca<2>(J, h, s); break;
-    case 3: launch_kernel_aca<3>(J, h, s); break;
-    case 4: launch_kernel_aca<4>(J, h, s); break;
-    default: launch_kernel_aca<0>(J, h, s); break;
+    case 1: teams_for(std::integral_constant<int, 1>{}); break;
+    case 2: teams_for(std::integral_constant<int, 2>{}); break;
+    case 3: teams_for(std::integral_constant<int, 3>{}); break;
+    case 4: teams_for(std::integral_constant<int, 4>{}); break;
+    default: teams_for(std::integral_constant<int, 0>{}); break;
+  }
+  if (ccount[kAcaCta] > 0) {
+    HM_CUDA(cudaEventRecord(h.ev_join, h.aux));
+    HM_CUDA(cudaStreamWaitEvent(s, h.ev_join, 0));
+  }
+  tr.mark("join", s);
+  if (tr.on)
+    std::fprintf(stderr, "[hm_trace] aca classes: %lld %lld %lld %lld %lld %lld\n", ccount[0], ccount[1], ccount[2],
+                 ccount[3], ccount[4], ccount[5]);
+  tr.dump();
+  tra.dump();
+  if (tr.on) {
+    unsigned long long ev[3 * kAcaClasses];
+    HM_CUDA(cudaMemcpyAsync(ev, evals.get(), sizeof(ev), cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+    for (int c = 0; c < kAcaCta; ++c)
+      std::fprintf(stderr, "[hm_trace] class %d: blocks %llu col-entries %.4g row-entries %.4g\n", c, ev[3 * c + 2],
+                   static_cast<double>(ev[3 * c]), static_cast<double>(ev[3 * c + 1]));
   }
   unsigned long long hrej = 0;
   HM_CUDA(cudaMemcpyAsync(&hrej, rej.get(), sizeof(hrej), cudaMemcpyDeviceToHost, s));

@@ -55,16 +55,28 @@ class DevBuf {
   }
   ~DevBuf() { reset(); }
 
+  // Large buffers (the stored operator: tens of GB) bypass the stream-ordered pool:
+  // measured on B200, cudaMallocAsync of 64 GB takes ~2 s and its free 2-9 s, while
+  // cudaMalloc maps the same in ~6 ms.  cudaFree synchronises the device, so a large
+  // buffer is never released under in-flight work.
+  static constexpr size_t kDirectBytes = size_t(256) << 20;
   void alloc(size_t count, cudaStream_t s) {
     reset();
     stream_ = s;
     n_ = count;
-    if (count) HM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), count * sizeof(T), s));
+    direct_ = count * sizeof(T) >= kDirectBytes;
+    if (!count) return;
+    if (direct_) HM_CUDA(cudaMalloc(reinterpret_cast<void**>(&p_), count * sizeof(T)));
+    else HM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), count * sizeof(T), s));
   }
   void reset() {
-    if (p_) cudaFreeAsync(p_, stream_);
+    if (p_) {
+      if (direct_) cudaFree(p_);
+      else cudaFreeAsync(p_, stream_);
+    }
     p_ = nullptr;
     n_ = 0;
+    direct_ = false;
   }
   void zero(cudaStream_t s) {
     if (n_) HM_CUDA(cudaMemsetAsync(p_, 0, n_ * sizeof(T), s));
@@ -81,10 +93,12 @@ class DevBuf {
     std::swap(p_, o.p_);
     std::swap(n_, o.n_);
     std::swap(stream_, o.stream_);
+    std::swap(direct_, o.direct_);
   }
   T* p_ = nullptr;
   size_t n_ = 0;
   cudaStream_t stream_ = nullptr;
+  bool direct_ = false;
 };
 
 inline unsigned grid_for(long long n, int threads, long long cap = 1ll << 30) {

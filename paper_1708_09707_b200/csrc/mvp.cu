@@ -924,8 +924,14 @@ void plan_far_field(HMatrix& h, cudaStream_t s) {
     }
   }
   if (h.cfg.precompute_aca) {
+    const auto t0 = std::chrono::steady_clock::now();
     h.U.alloc(std::max(uo[hi] - uo[lo], 1ll), s);
     h.V.alloc(std::max(vo[hi] - vo[lo], 1ll), s);
+    if (std::getenv("HM_TRACE")) {
+      HM_CUDA(cudaStreamSynchronize(s));
+      std::fprintf(stderr, "[hm_trace] U/V alloc %.1f GB: %.3f ms\n", 8.0 * (uo[hi] - uo[lo] + vo[hi] - vo[lo]) / 1e9,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
     compute_aca(h, lo, hi, s);
     h.factors_valid = true;
     // S_l with the achieved ranks

@@ -180,3 +180,26 @@ def test_halton_and_force_dense(gpu, oracle):
     assert h.stats()["n_aca"] == 0
     x = symmetric(11, 512)
     assert np.array_equal(bits(h.mvp(x)), bits(o.mvp(x)))
+
+
+@pytest.mark.parametrize("n,d,c_leaf,kind,k", [
+    (1 << 16, 2, 64, 0, 16),   # noise-floor rejections in every size class
+    (5000, 3, 40, 0, 24),      # k > 16: the 32-wide register rank window
+    (6000, 2, 100, 1, 12),     # Matern, non-power-of-two clusters up to 750 wide
+])
+def test_aca_size_classes_bitwise(built, n, d, c_leaf, kind, k):
+    """Every ACA size class (team kernels for max(m,n) <= 64/128/256/512, the CTA kernel
+    beyond) reproduces aca_batched's pivots, ranks and factors bit for bit."""
+    P, h, o = built(n, d, c_leaf, kind, k=k)
+    r0 = h.stats()["aca_rejections"]
+    fh = h.aca_factors()
+    rej = h.stats()["aca_rejections"] - r0
+    fo = o.aca_all()
+    assert np.array_equal(fh["k_eff"], fo["k_eff"])
+    assert np.array_equal(fh["row_piv"], fo["row_piv"])
+    assert np.array_equal(fh["col_piv"], fo["col_piv"])
+    assert rej == int(fo["rejections"].sum())
+    for a, b in zip(fh["u"], fo["u"]):
+        assert np.array_equal(bits(a), bits(b))
+    for a, b in zip(fh["v"], fo["v"]):
+        assert np.array_equal(bits(a), bits(b))
