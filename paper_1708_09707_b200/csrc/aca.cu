@@ -980,13 +980,24 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
       {
         double yp[DIM > 0 ? DIM : 20];
         E.load(rl + p, yp);
+        double uP[KC];  // u_l[p], right-aligned (aca_chain.cuh)
+#pragma unroll
+        for (int j = 0; j < KC; ++j) uP[j] = j >= KC - r ? s_up[j - (KC - r)] : 0.0;
         for (int j = t; j < n; j += TT) {
           double a;
           if (j >= next && j < next + filled) {
             a = s_win[(j % W) * PS + p];
           } else {
-            a = E.eval(yp, cl + j);
-            for (int l = 0; l < r; ++l) a = hsub(a, hmul(s_up[l], vat(l, j)));
+            const double* vb;
+            int vs;
+            if constexpr (VSM) {
+              vb = s_v + static_cast<long long>(r - KC) * NCAP + j;
+              vs = NCAP;
+            } else {
+              vb = V + static_cast<long long>(j) * kmax + (r - KC);
+              vs = 1;
+            }
+            a = Chain<KC>::run(E.eval(yp, cl + j), uP, r, vb, vs);
           }
           vat(r, j) = a;
         }
@@ -1065,6 +1076,262 @@ void launch_win(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, cudaS
   HM_LAUNCH_CHECK();
 }
 
+// ---------------------------------------------------------------------------
+// Big-block kernel (max(m, n) > 1024): one 256-thread CTA per block, rows strided
+// over the CTA in pairs.  The window of W candidate columns lives in a per-CTA
+// global scratch (L2-resident: W x m doubles); for each row pair a thread loads
+// u_l of its two rows from the U factor into right-aligned registers once and
+// reuses them for every fresh window column (Chain<KC>::run2), so the chain costs
+// one broadcast v load per step as in the window kernels.  Pivot rows are a
+// shared bitmask.  Same semantics and bits as the window kernels.
+constexpr int kBigThreads = 256;
+constexpr int kBigW = 8;
+
+template <int DIM, int KIND, int KC>
+__global__ void __launch_bounds__(kBigThreads) aca_big_kernel(AcaJob J, KernelEntry<DIM, KIND> E, double* gscratch,
+                                                              long long gstride, int mask_words) {
+  constexpr int TT = kBigThreads;
+  constexpr int W = kBigW;
+  constexpr int G = TT / W;  // 32: one warp per column in the qualification pass
+  constexpr int YD = DIM > 0 ? DIM : 20;
+  extern __shared__ double smem[];
+  unsigned* s_mask = reinterpret_cast<unsigned*>(smem);
+  double* s_up = smem + (mask_words + 1) / 2;  // kKmax
+  double* s_rbv = s_up + kKmax;                // 8 warps
+  int* s_rbi = reinterpret_cast<int*>(s_rbv + 8);
+  int* s_state = reinterpret_cast<int*>(s_rbv + 12);
+  double* s_misc = s_rbv + 20;  // [0] job [1] scale [2] verdict
+  const int t = threadIdx.x, lane = t & 31, wib = t >> 5;
+  const double kEps0sq = 1e-14 * 1e-14;
+  const int kmax = J.kmax;
+  double* win = gscratch + static_cast<long long>(blockIdx.x) * gstride * W;
+
+  for (;;) {
+    if (t == 0) s_misc[0] = static_cast<double>(atomicAdd(J.counter, 1));
+    __syncthreads();
+    const long long job = static_cast<long long>(s_misc[0]);
+    if (job >= J.njobs) return;
+    const int b = J.order[job];
+    const int rl = J.rl[b], m = J.m[b], cl = J.cl[b], n = J.nn[b];
+    double* U = J.U + (J.u_off[b] - J.u_base);
+    double* V = J.V + (J.v_off[b] - J.v_base);
+    const int tsh = J.tile_shift;
+    auto uix = [&](int l, int i) -> long long {
+      if (tsh < 0) return static_cast<long long>(l) * m + i;
+      return ((static_cast<long long>(i >> tsh) * kmax + l) << tsh) + (i & ((1 << tsh) - 1));
+    };
+    const long long PS = gstride;
+    for (int i = t; i < (m + 31) / 32; i += TT) s_mask[i] = 0u;
+    __syncthreads();
+    auto is_used = [&](int i) -> bool { return (s_mask[i >> 5] >> (i & 31)) & 1u; };
+
+    int next = 0, filled = 0, k_eff = 0;
+    unsigned long long rejections = 0, ev_col = 0, ev_row = 0;
+    double scale = -1.0;
+    const double gm = static_cast<double>(m) * 1.2e-16;
+
+    for (int r = 0; r < kmax; ++r) {
+      int acc_w = -1;
+      while (next < n) {
+        const int wcols = min(W, n - next);
+        ev_col += static_cast<unsigned long long>(wcols - filled) * m;
+        // fill: per row pair, u of the two rows into registers once, then every fresh column
+        for (int i0 = t; i0 < m; i0 += 2 * TT) {
+          const int i1 = i0 + TT;
+          const bool ok1 = i1 < m;
+          double uR[2][KC];
+#pragma unroll
+          for (int j = 0; j < KC; ++j) {
+            const int l = j - (KC - r);
+            uR[0][j] = l >= 0 ? U[uix(l, i0)] : 0.0;
+            uR[1][j] = (l >= 0 && ok1) ? U[uix(l, i1)] : 0.0;
+          }
+          double y0[YD], y1[YD];
+          E.load(rl + i0, y0);
+          E.load(rl + (ok1 ? i1 : i0), y1);
+          for (int co = filled; co < wcols; ++co) {
+            const int col = next + co;
+            double a0 = E.eval(y0, cl + col);
+            double a1 = ok1 ? E.eval(y1, cl + col) : 0.0;
+            Chain<KC>::run2(a0, a1, uR[0], uR[1], r, V + static_cast<long long>(col) * kmax + (r - KC), 1);
+            double* dst = win + static_cast<long long>(col % W) * PS;
+            dst[i0] = a0;
+            if (ok1) dst[i1] = a1;
+          }
+        }
+        filled = wcols;
+        __syncthreads();
+        {
+          const int w = wib;  // G == 32: warp w scans window column w
+          double sum = 0.0;
+          int nz = 0;
+          if (w < wcols) {
+            const double* src = win + static_cast<long long>((next + w) % W) * PS;
+            for (int i = lane; i < m; i += 32) {
+              const double a = src[i];
+              sum = hadd(sum, hmul(a, a));
+              nz |= (!is_used(i) && fabs(a) > 0.0) ? 1 : 0;
+            }
+          }
+#pragma unroll
+          for (int o = 16; o; o >>= 1) {
+            sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+            nz |= __shfl_xor_sync(0xffffffffu, nz, o);
+          }
+          if (lane == 0 && w < wcols) {
+            int st = 0;
+            if (nz) {
+              if (scale < 0.0) {
+                st = 1;
+              } else {
+                const double T = hmul(kEps0sq, scale);
+                const double lo = hmul(sum, 1.0 - 4.0 * gm), hi = hmul(sum, 1.0 + 4.0 * gm);
+                st = lo > T ? 1 : (hi <= T ? 0 : 2);
+              }
+            }
+            s_state[w] = st;
+          }
+        }
+        __syncthreads();
+        for (int w = 0; w < wcols; ++w) {
+          int st = s_state[w];
+          if (st == 2) {
+            if (t == 0) {
+              const double* src = win + static_cast<long long>((next + w) % W) * PS;
+              double f = hmul(src[0], src[0]);
+              for (int i = 1; i < m; ++i) f = hadd(f, hmul(src[i], src[i]));
+              s_misc[2] = f > hmul(kEps0sq, scale) ? 1.0 : 0.0;
+            }
+            __syncthreads();
+            st = s_misc[2] != 0.0 ? 1 : 0;
+            __syncthreads();
+          }
+          if (st == 1) {
+            acc_w = w;
+            break;
+          }
+        }
+        const int consumed = acc_w >= 0 ? acc_w + 1 : wcols;
+        rejections += static_cast<unsigned long long>(acc_w >= 0 ? acc_w : wcols);
+        next += consumed;
+        filled = acc_w >= 0 ? wcols - consumed : 0;
+        if (acc_w >= 0) break;
+      }
+      if (acc_w < 0) break;
+      const int cstar = next - 1;
+      const double* acol = win + static_cast<long long>(cstar % W) * PS;
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+      for (int i = t; i < m; i += TT) {
+        if (!is_used(i)) {
+          const double av = fabs(acol[i]);
+          if (av > bv) {
+            bv = av;
+            bi = i;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        argmax_combine(bv, bi, ov, oi);
+      }
+      if (lane == 0) {
+        s_rbv[wib] = bv;
+        s_rbi[wib] = bi;
+      }
+      __syncthreads();
+      bv = s_rbv[0];
+      bi = s_rbi[0];
+      for (int g = 1; g < TT / 32; ++g) argmax_combine(bv, bi, s_rbv[g], s_rbi[g]);
+      const int p = bi;
+      if (t == 0) {
+        if (r == 0) {
+          double f = hmul(acol[0], acol[0]);
+          for (int i = 1; i < m; ++i) f = hadd(f, hmul(acol[i], acol[i]));
+          s_misc[1] = f;
+        }
+        for (int l = 0; l < r; ++l) s_up[l] = U[uix(l, p)];
+      }
+      __syncthreads();
+      if (r == 0) scale = s_misc[1];
+      const double pivot_val = acol[p];
+      for (int i = t; i < m; i += TT) U[uix(r, i)] = __ddiv_rn(acol[i], pivot_val);
+      ev_row += n;
+      {
+        double yp[YD];
+        E.load(rl + p, yp);
+        double uP[KC];  // u_l[p], right-aligned: every V-row load of the chain issues up front
+#pragma unroll
+        for (int j = 0; j < KC; ++j) uP[j] = j >= KC - r ? s_up[j - (KC - r)] : 0.0;
+        for (int j = t; j < n; j += TT) {
+          double a;
+          if (j >= next && j < next + filled) {
+            a = win[static_cast<long long>(j % W) * PS + p];
+          } else {
+            a = Chain<KC>::run(E.eval(yp, cl + j), uP, r, V + static_cast<long long>(j) * kmax + (r - KC), 1);
+          }
+          V[static_cast<long long>(j) * kmax + r] = a;
+        }
+      }
+      __syncthreads();
+      if (t == 0) s_mask[p >> 5] |= 1u << (p & 31);
+      for (int co = 0; co < filled; ++co) {
+        const int col = next + co;
+        const double vr = V[static_cast<long long>(col) * kmax + r];
+        double* dst = win + static_cast<long long>(col % W) * PS;
+        for (int i = t; i < m; i += TT) dst[i] = hsub(dst[i], hmul(U[uix(r, i)], vr));
+      }
+      if (t == 0) {
+        J.row_piv[static_cast<long long>(b) * kmax + r] = p;
+        J.col_piv[static_cast<long long>(b) * kmax + r] = cstar;
+      }
+      k_eff = r + 1;
+    }
+    for (int l = k_eff; l < kmax; ++l)
+      for (int i = t; i < m; i += TT) U[uix(l, i)] = 0.0;
+    if (k_eff < kmax) {
+      for (int idx = t; idx < n * (kmax - k_eff); idx += TT) {
+        const int j = idx / (kmax - k_eff), l = k_eff + idx % (kmax - k_eff);
+        V[static_cast<long long>(j) * kmax + l] = 0.0;
+      }
+    }
+    for (int l = k_eff + t; l < kmax; l += TT) {
+      J.row_piv[static_cast<long long>(b) * kmax + l] = -1;
+      J.col_piv[static_cast<long long>(b) * kmax + l] = -1;
+    }
+    if (t == 0) {
+      J.k_eff[b] = k_eff;
+      if (J.rejections && rejections) atomicAdd(J.rejections, rejections);
+      if (J.evals) {
+        atomicAdd(J.evals, ev_col);
+        atomicAdd(J.evals + 1, ev_row);
+        atomicAdd(J.evals + 2, 1ull);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int DIM, int KIND, int KC>
+void launch_big(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int max_rows, int sms, cudaStream_t s) {
+  if (J.njobs <= 0) return;
+  const int mask_words = (max_rows + 31) / 32;
+  const size_t smem = ((mask_words + 1) / 2 + kKmax + 40) * sizeof(double);
+  auto kfn = aca_big_kernel<DIM, KIND, KC>;
+  HM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int occ = 0;
+  HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kBigThreads, smem));
+  const long long ctas = std::min<long long>(J.njobs, static_cast<long long>(std::max(occ, 1)) * sms);
+  // per-CTA window of kBigW columns (L2-resident)
+  DevBuf<double> scratch;
+  const long long gstride = max_rows + 1;
+  scratch.alloc(static_cast<size_t>(gstride) * kBigW * ctas, s);
+  kfn<<<static_cast<unsigned>(std::max(ctas, 1ll)), kBigThreads, smem, s>>>(J, E, scratch.get(), gstride, mask_words);
+  HM_LAUNCH_CHECK();
+}
+
 constexpr int kTeamW = 4;  // candidate columns per wave
 
 template <int DIM, int KIND, int NW, int KC>
@@ -1083,12 +1350,13 @@ void launch_team(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, cuda
 
 // ACA size classes: team kernels for max(m, n) <= 64 * NW (NW = 1, 2, 4, 8), the
 // CTA kernel for larger blocks, for k > 32 and for the epsilon criterion.
-constexpr int kAcaClasses = 6;
-constexpr int kAcaCta = kAcaClasses - 1;  // the CTA kernel's class
+constexpr int kAcaClasses = 7;
+constexpr int kAcaBig = 5;                // aca_big_kernel
+constexpr int kAcaCta = kAcaClasses - 1;  // the general CTA kernel (epsilon criterion, k > 32)
 __host__ __device__ inline int aca_class(int m, int n, long long kmax, bool has_eps) {
   if (has_eps || kmax > 32) return kAcaCta;
   const int c = m > n ? m : n;
-  return c <= 64 ? 0 : c <= 128 ? 1 : c <= 256 ? 2 : c <= 512 ? 3 : c <= 1024 ? 4 : kAcaCta;
+  return c <= 64 ? 0 : c <= 128 ? 1 : c <= 256 ? 2 : c <= 512 ? 3 : c <= 1024 ? 4 : kAcaBig;
 }
 
 __global__ void class_key_kernel(const int* __restrict__ m, const int* __restrict__ nn, long long begin, long long cnt,
@@ -1202,25 +1470,62 @@ void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStrea
     return Jc;
   };
   // large blocks on the auxiliary stream, concurrently with the team kernels
+  // the CTA kernel (largest blocks first, long per-block latency) runs first, on the
+  // same stream: sharing SMs with the window kernels starves their 1-CTA/SM launches
+  const bool cta_aux = std::getenv("HM_ACA_AUX") != nullptr;
+  cudaStream_t sc = cta_aux ? h.aux : s;
   if (ccount[kAcaCta] > 0) {
-    HM_CUDA(cudaEventRecord(h.ev_fork, s));
-    HM_CUDA(cudaStreamWaitEvent(h.aux, h.ev_fork, 0));
-    const AcaJob Jb = sub(kAcaCta);
-    tra.mark("start", h.aux);
-    switch (h.d) {
-      case 1: launch_kernel_aca<1>(Jb, h, h.aux); break;
-      case 2: launch_kernel_aca<2>(Jb, h, h.aux); break;
-      case 3: launch_kernel_aca<3>(Jb, h, h.aux); break;
-      case 4: launch_kernel_aca<4>(Jb, h, h.aux); break;
-      default: launch_kernel_aca<0>(Jb, h, h.aux); break;
+    if (cta_aux) {
+      HM_CUDA(cudaEventRecord(h.ev_fork, s));
+      HM_CUDA(cudaStreamWaitEvent(h.aux, h.ev_fork, 0));
     }
-    tra.mark("cta kernel (>512, aux)", h.aux);
+    const AcaJob Jb = sub(kAcaCta);
+    tra.mark("start", sc);
+    switch (h.d) {
+      case 1: launch_kernel_aca<1>(Jb, h, sc); break;
+      case 2: launch_kernel_aca<2>(Jb, h, sc); break;
+      case 3: launch_kernel_aca<3>(Jb, h, sc); break;
+      case 4: launch_kernel_aca<4>(Jb, h, sc); break;
+      default: launch_kernel_aca<0>(Jb, h, sc); break;
+    }
+    tra.mark("cta kernel (>1024)", sc);
+    if (!cta_aux) tr.mark("cta kernel (>1024)", s);
   }
   auto teams_kind = [&](auto dimc, auto kindc) {
     constexpr int DIM = decltype(dimc)::value;
     constexpr int KIND = decltype(kindc)::value;
     KernelEntry<DIM, KIND> E{h.coords.get(), h.n, h.d, h.kp};
     const bool team = std::getenv("HM_ACA_TEAM") != nullptr;  // A/B: register-window kernels
+    if (ccount[kAcaBig] > 0) {
+      int max_rows = 0;
+      for (long long b = leaf_begin; b < leaf_end; ++b)
+        if (aca_class(h.aca.h_m[b], h.aca.h_n[b], h.cfg.k, eps) == kAcaBig) max_rows = std::max(max_rows, h.aca.h_m[b]);
+      if (tr.on && std::getenv("HM_TRACE_BIG")) {  // per-size sub-launches (jobs are sorted by n descending)
+        const int edges[] = {1 << 30, 16384, 8192, 4096, 2048, 0};
+        AcaJob Jb = sub(kAcaBig);
+        long long off = 0;
+        for (int e = 0; e < 5; ++e) {
+          long long c = 0;
+          for (long long b = leaf_begin; b < leaf_end; ++b)
+            if (aca_class(h.aca.h_m[b], h.aca.h_n[b], h.cfg.k, eps) == kAcaBig && h.aca.h_n[b] < edges[e] &&
+                h.aca.h_n[b] >= edges[e + 1])
+              ++c;
+          AcaJob Je = Jb;
+          Je.order = Jb.order + off;
+          Je.njobs = c;
+          HM_CUDA(cudaMemsetAsync(Je.counter, 0, sizeof(int), s));
+          if (c) launch_big<DIM, KIND, 16>(Je, E, max_rows, sms, s);
+          static char names[5][48];
+          std::snprintf(names[e], sizeof(names[e]), "big n in [%d,%d): %lld", edges[e + 1], edges[e], c);
+          tr.mark(names[e], s);
+          off += c;
+        }
+      } else {
+        if (h.cfg.k <= 16) launch_big<DIM, KIND, 16>(sub(kAcaBig), E, max_rows, sms, s);
+        else launch_big<DIM, KIND, 32>(sub(kAcaBig), E, max_rows, sms, s);
+        tr.mark("big (>1024)", s);
+      }
+    }
     if (h.cfg.k <= 16) {
       const char* v16 = std::getenv("HM_W16");
       const char* v8 = std::getenv("HM_W8");
@@ -1260,21 +1565,21 @@ void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStrea
     case 4: teams_for(std::integral_constant<int, 4>{}); break;
     default: teams_for(std::integral_constant<int, 0>{}); break;
   }
-  if (ccount[kAcaCta] > 0) {
+  if (ccount[kAcaCta] > 0 && cta_aux) {
     HM_CUDA(cudaEventRecord(h.ev_join, h.aux));
     HM_CUDA(cudaStreamWaitEvent(s, h.ev_join, 0));
   }
   tr.mark("join", s);
   if (tr.on)
-    std::fprintf(stderr, "[hm_trace] aca classes: %lld %lld %lld %lld %lld %lld\n", ccount[0], ccount[1], ccount[2],
-                 ccount[3], ccount[4], ccount[5]);
+    std::fprintf(stderr, "[hm_trace] aca classes: %lld %lld %lld %lld %lld %lld %lld\n", ccount[0], ccount[1],
+                 ccount[2], ccount[3], ccount[4], ccount[5], ccount[6]);
   tr.dump();
   tra.dump();
   if (tr.on) {
     unsigned long long ev[3 * kAcaClasses];
     HM_CUDA(cudaMemcpyAsync(ev, evals.get(), sizeof(ev), cudaMemcpyDeviceToHost, s));
     HM_CUDA(cudaStreamSynchronize(s));
-    for (int c = 0; c < kAcaCta; ++c)
+    for (int c = 0; c < kAcaClasses; ++c)
       std::fprintf(stderr, "[hm_trace] class %d: blocks %llu col-entries %.4g row-entries %.4g\n", c, ev[3 * c + 2],
                    static_cast<double>(ev[3 * c]), static_cast<double>(ev[3 * c + 1]));
   }

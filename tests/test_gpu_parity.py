@@ -186,10 +186,11 @@ def test_halton_and_force_dense(gpu, oracle):
     (1 << 16, 2, 64, 0, 16),   # noise-floor rejections in every size class
     (5000, 3, 40, 0, 24),      # k > 16: the 32-wide register rank window
     (6000, 2, 100, 1, 12),     # Matern, non-power-of-two clusters up to 750 wide
+    (60000, 1, 64, 0, 16),     # d = 1: blocks of 15000 rows (global window column of the big kernel)
 ])
 def test_aca_size_classes_bitwise(built, n, d, c_leaf, kind, k):
-    """Every ACA size class (team kernels for max(m,n) <= 64/128/256/512, the CTA kernel
-    beyond) reproduces aca_batched's pivots, ranks and factors bit for bit."""
+    """Every ACA size class (window kernels for max(m,n) <= 64/128/256/512/1024, the
+    big-block kernel beyond) reproduces aca_batched's pivots, ranks and factors bit for bit."""
     P, h, o = built(n, d, c_leaf, kind, k=k)
     r0 = h.stats()["aca_rejections"]
     fh = h.aca_factors()

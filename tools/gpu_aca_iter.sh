@@ -2,4 +2,3 @@
 set -x
 timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "aca or mvp_matches or c1_norm" > gpurun_out/pytest_aca.log 2>&1; tail -3 gpurun_out/pytest_aca.log
 python tools/trace_build.py 2>&1 | tail -18
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'aca_win' -s 0 -c 2 -o gpurun_out/prof_win python tools/trace_build.py > gpurun_out/ncu_win.log 2>&1; tail -2 gpurun_out/ncu_win.log
