@@ -228,7 +228,7 @@ def run_ours(args):
         S_lm = float((f["k_eff"] * (lv[:, 1] - lv[:, 0])).sum())
         S_ln = S_l - S_lm
     flops = 2.0 * (S_d + S_l)
-    alg_bytes = 8.0 * (S_d + S_l + 2 * n)
+    alg_bytes = 8.0 * (S_d + S_l + 2 * n)  # the reference layout's bytes (every dense block stored)
 
     # inputs resident in HBM
     xs = [torch.from_numpy(symmetric(43 + t, n)).cuda() for t in range(4)]
@@ -270,21 +270,41 @@ def run_ours(args):
         h.mvp_device(xs[t % 4].data_ptr(), z.data_ptr(), sptr)
     barrier()
     prof = h.profile_end()
-    rows_ms, rows_cnt = prof.get("rows", (0.0, 0))
-    rows_avg = rows_ms / max(rows_cnt, 1)
-    # algorithmic bytes of the row-gather kernel on this rank: stored dense blocks + U
-    # (k_eff x m per admissible leaf) + z write; the t kernel streams V (k_eff x n)
-    rows_bytes = 8.0 * (st["S_d_own"] + st["S_lm"] + (st["row_end"] - st["row_begin"]))
+    # algorithmic bytes per launch of each product kernel on this rank:
+    #   near_pairs: stored near-field blocks + the partial products it writes (+ x segments)
+    #   lowrank_t : V (k_eff x n per admissible leaf) + t writes
+    #   rows      : U tiles (k_eff x S) + the dense partials (symmetric) or stored blocks + z
+    S = n >> int(st["dmax_leaf"])
+    own_rows = st["row_end"] - st["row_begin"]
+    sym = bool(st.get("near_sym", 0))
+    n_dense_own = st["S_d_own"] / float(S * S) if sym else 0.0
+    kbytes = {
+        "near_pairs": 8.0 * (st["S_d_stored"] + n_dense_own * S + 2.0 * S * n_dense_own / 2.0),
+        "lowrank_t": 8.0 * (st["S_ln"] + st["n_aca"] * args.k),
+        "rows": 8.0 * ((n_dense_own * S if sym else st["S_d_own"]) + st["S_lm"] + own_rows),
+    }
     hbm_peak, peak_kind = peaks()
-    rows_gbs = rows_bytes / (rows_avg * 1e-3) / 1e9 if rows_avg > 0 else None
+    kern = {}
+    for name, nb in kbytes.items():
+        ms_tot, cnt = prof.get(name, (0.0, 0))
+        if cnt:
+            avg = ms_tot / cnt
+            kern[name] = {"avg_ms": avg, "alg_bytes": nb, "gbs": nb / (avg * 1e-3) / 1e9}
+    dom = max(kern, key=lambda k: kern[k]["avg_ms"]) if kern else None
+    moved_bytes = sum(kbytes.values()) + 32.0 * n  # + gather x / scatter z
+    names = {"rows": "rows_tma_kernel (row-cluster product: U tiles + dense partials, TMA ring)",
+             "lowrank_t": "t_pair_kernel (t = V^T x, TMA ring, two leaves per warp)",
+             "near_pairs": "near_pair_kernel (symmetric stored near field, both leaves of a pair)"}
     traffic = None  # dram bytes per launch of the dominant kernel, from the committed ncu capture
     try:
         with open(os.path.join(REPO, "profiles", "traffic_c2.json")) as f:
             tr = json.load(f)
         c = tr["config"]
-        if (c["n"], c["d"], c["c_leaf"], c["k"], c["mode"]) == (n, d, args.c_leaf, args.k, args.mode) and world == 1:
-            kk = next(v for k, v in tr["kernels"].items() if k.startswith("rows"))
-            traffic = kk["dram_read_bytes"] + kk["dram_write_bytes"]
+        if (c["n"], c["d"], c["c_leaf"], c["k"], c["mode"], c.get("near_sym", False)) == \
+                (n, d, args.c_leaf, args.k, args.mode, sym) and world == 1 and dom:
+            kk = tr["kernels"].get(dom)
+            if kk:
+                traffic = kk["dram_read_bytes"] + kk["dram_write_bytes"]
     except Exception:  # noqa: BLE001
         traffic = None
     launches_per_step = sum(c for (_, c) in prof.values()) / prof_steps
@@ -332,15 +352,19 @@ def run_ours(args):
                        "n": n, "d": d, "c_leaf": args.c_leaf, "k": args.k, "mode": args.mode,
                        "parallelism": f"row-cluster x{world}" if world > 1 else "single",
                        "l2": f"no flush: stored operator {alg_bytes / 1e9:.1f} GB >> 126 MB L2"},
-            "hbm_gbs": hbm, "build_s": build_s,
+            "hbm_gbs": moved_bytes / (ms_step * 1e-3) / 1e9, "hbm_gbs_reference_layout": hbm, "build_s": build_s,
             "build_phases_ms": {k: tms[k] for k in ("morton_ms", "tree_ms", "aca_ms", "near_ms", "setup_ms")},
-            "work": {"S_d": S_d, "S_l": S_l, "S_lm": S_lm, "S_ln": S_ln, "flops_per_step": flops,
+            "work": {"S_d": S_d, "S_d_stored": st["S_d_stored"], "near_sym": sym, "S_l": S_l, "S_lm": S_lm,
+                     "S_ln": S_ln, "flops_per_step": flops, "moved_bytes_per_step": moved_bytes,
                      "alg_bytes_per_step": alg_bytes, "n_dense": st["n_dense"], "n_aca": st["n_aca"],
                      "aca_rejections": st["aca_rejections"]},
-            "roofline": {"bound": "hbm", "kernel": "rows_tma_kernel (near + far row-cluster product, TMA ring)",
-                         "achieved": rows_gbs, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": (rows_gbs / hbm_peak) if rows_gbs else None, "traffic": traffic,
-                         "peak_kind": peak_kind, "alg_bytes_per_launch": rows_bytes, "avg_ms": rows_avg},
+            "roofline": {"bound": "hbm", "kernel": names.get(dom, dom),
+                         "achieved": kern[dom]["gbs"] if dom else None, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": (kern[dom]["gbs"] / hbm_peak) if dom else None, "traffic": traffic,
+                         "peak_kind": peak_kind, "alg_bytes_per_launch": kern[dom]["alg_bytes"] if dom else None,
+                         "avg_ms": kern[dom]["avg_ms"] if dom else None,
+                         "kernels": {k: {"gbs": v["gbs"], "frac": v["gbs"] / hbm_peak, "avg_ms": v["avg_ms"],
+                                         "alg_bytes": v["alg_bytes"]} for k, v in kern.items()}},
             "kernels_ms_per_step": {k: v[0] / max(v[1], 1) * (v[1] / prof_steps) for k, v in prof.items()},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},

@@ -76,6 +76,8 @@ typedef struct {
   int32_t dmax_leaf;
   int64_t row_begin, row_end;
   double device_bytes;
+  double S_d_stored;       /* dense entries actually stored (symmetric near field: about half) */
+  int32_t near_sym;        /* 1: symmetric near-field storage + pair kernel in use */
 } hm_stats;
 
 const char* hm_last_error(void);

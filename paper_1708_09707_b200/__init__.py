@@ -74,7 +74,8 @@ class _Timings(C.Structure):
 class _Stats(C.Structure):
     _fields_ = [("n_dense", _i64), ("n_aca", _i64), ("S_d", _d), ("S_l", _d), ("sum_m_adm", _d),
                 ("sum_n_adm", _d), ("S_lm", _d), ("S_ln", _d), ("S_d_own", _d), ("aca_rejections", _i64), ("dmax_leaf", _i32), ("row_begin", _i64),
-                ("row_end", _i64), ("device_bytes", _d)]
+                ("row_end", _i64), ("device_bytes", _d),
+                ("S_d_stored", _d), ("near_sym", _i32)]
 
 
 def _sig(name, res, args):
@@ -123,7 +124,7 @@ EXPORTED_SYMBOLS = [
     "hm_exp_port_device", "hm_log_port_host", "hm_log_port_device", "hm_profile_begin", "hm_profile_end",
 ]
 
-KERNEL_IDS = ["gather_x", "lowrank_t", "rows", "scatter_z", "aca", "rows_far", "allgather", "unused"]
+KERNEL_IDS = ["gather_x", "lowrank_t", "rows", "scatter_z", "aca", "rows_far", "allgather", "near_pairs"]
 
 
 def _check(rc: int) -> None:

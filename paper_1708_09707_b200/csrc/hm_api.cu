@@ -607,6 +607,8 @@ hm_status hm_get_stats(hm_handle* H, hm_stats* st) {
     st->row_begin = h.row_begin;
     st->row_end = h.row_end;
     st->device_bytes = static_cast<double>(h.dense_vals.bytes() + h.U.bytes() + h.V.bytes() + h.coords.bytes());
+    st->S_d_stored = h.S_d_stored;
+    st->near_sym = h.near_sym ? 1 : 0;
   });
 }
 

@@ -39,7 +39,8 @@ struct LeafList {
 // Per-kernel CUDA-event clock (enabled by hm_profile_begin): events are recorded on
 // the launching stream around each launch and summed at hm_profile_end.
 enum KernelId : int {
-  kKGather = 0, kKLowrankT = 1, kKRows = 2, kKScatter = 3, kKAca = 4, kKRowsFar = 5, kKAllgather = 6, kKNum = 8
+  kKGather = 0, kKLowrankT = 1, kKRows = 2, kKScatter = 3, kKAca = 4, kKRowsFar = 5, kKAllgather = 6,
+  kKNearPairs = 7, kKNum = 8
 };
 struct KClock {
   bool on = false;
@@ -113,6 +114,16 @@ struct HMatrix {
   // stored near field: column-major blocks
   DevBuf<long long> dense_off;
   DevBuf<double> dense_vals;
+  // Symmetric near field (regular geometry, TMA product): A(sigma,tau) = A(tau,sigma)^T
+  // bitwise (dx^2 is sign-symmetric), so only blocks with row.lower <= col.lower are
+  // stored.  The pair kernel streams each stored block once and writes the per-leaf
+  // dense products of BOTH leaves of the pair into part (S doubles per dense leaf);
+  // the row product then folds those partials in leaf order (hmatrix.cpp:80-104).
+  bool near_sym = false;
+  long long n_pairs = 0;
+  DevBuf<int> pair_leaf, pair_mirror;  // stored leaf, mirror leaf (-1: diagonal or not own)
+  DevBuf<int4> pair_desc;              // {leaf, first stored column, col.lower, row.lower}
+  DevBuf<double> part;
 
   // product workspaces
   DevBuf<double> xm, zm, xin, zout;
@@ -121,6 +132,7 @@ struct HMatrix {
   // algorithmic sizes
   double S_d = 0, sum_m_adm = 0, sum_n_adm = 0, S_l = 0, S_lm = 0, S_ln = 0;
   double S_d_own = 0;  // dense entries of the rows this rank owns
+  double S_d_stored = 0;  // dense entries stored (near_stored; about S_d_own / 2 when near_sym)
   Timings tm;
   KClock clk;
 

@@ -13,8 +13,11 @@
 // Stored dense blocks are column-major (entry (i,j) at j*m + i) so the threads
 // of a row cluster stream each block with fully coalesced 256-B warp loads;
 // U is rank-major (coalesced over i), V interleaved n x k (coalesced over l).
+#include <cuda.h>
+
 #include <algorithm>
 #include <chrono>
+#include <string>
 #include <vector>
 
 #include "hmatrix.h"
@@ -40,13 +43,15 @@ __global__ void scatter_z_kernel(const double* __restrict__ zm, const long long*
     z[perm[i]] = zm[i];  // permute_vector Inverse
 }
 
-// stored near field: column-major blocks
+// stored near field: column-major blocks (leaves list[q], q < cnt; list == nullptr: lo + q)
 template <int DIM>
 __global__ void store_dense_kernel(const double* __restrict__ coords, long long n, int d, KernelParams kp,
                                    const int* __restrict__ rl, const int* __restrict__ m, const int* __restrict__ cl,
                                    const int* __restrict__ nn, long long leaf_begin, long long leaf_end,
-                                   const long long* __restrict__ off, long long off_base, double* __restrict__ vals) {
-  for (long long b = leaf_begin + blockIdx.x; b < leaf_end; b += gridDim.x) {
+                                   const long long* __restrict__ off, long long off_base, double* __restrict__ vals,
+                                   const int* __restrict__ list) {
+  for (long long q = leaf_begin + blockIdx.x; q < leaf_end; q += gridDim.x) {
+    const long long b = list ? list[q] : q;
     const int r0 = rl[b], mb = m[b], c0 = cl[b], nb = nn[b];
     double* out = vals + (off[b] - off_base);
     const long long total = static_cast<long long>(mb) * nb;
@@ -272,10 +277,142 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
+// symmetric near field: mirror of every own stored leaf by binary search in the
+// canonical (row.lower, col.lower) order of equal-depth dense leaves
+__global__ void mirror_kernel(const int* __restrict__ list, long long cnt, const int* __restrict__ rl,
+                              const int* __restrict__ cl, long long ndense, long long row_begin, long long row_end,
+                              int* __restrict__ mirror) {
+  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < cnt;
+       q += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int L = list[q];
+    const int r0 = rl[L], c0 = cl[L];
+    int res = -1;
+    if (c0 > r0 && c0 >= row_begin && c0 < row_end) {
+      long long lo = 0, hi = ndense;
+      while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        const int a = rl[mid], b = cl[mid];
+        if (a < c0 || (a == c0 && b < r0)) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo < ndense && rl[lo] == c0 && cl[lo] == r0) res = static_cast<int>(lo);
+    }
+    mirror[q] = res;
+  }
+}
+
+// One CTA of S threads per stored S x S block B (column-major, rows tau, cols sigma).
+// The block is streamed ONCE by TMA tensor copies (cp.async.bulk.tensor.2d, box =
+// 16 rows x S columns, SWIZZLE_128B) into a ring of NST stages; the 128-byte swizzle
+// makes both walks cheap: thread t folds
+//   y_tau[t]   = ((0 + B(t,0) x_s[0]) + B(t,1) x_s[1]) + ...   (leaf (tau,sigma), row walk)
+//   y_sigma[t] = ((0 + B(0,t) x_t[0]) + B(1,t) x_t[1]) + ...   (leaf (sigma,tau), column walk)
+// as two independent chains in one loop, both in the reference's sequential order
+// (dense_blocks.cpp:101-116).  Diagonal blocks (and pairs whose mirror another rank
+// owns) fold only the first.
+template <int S>
+__device__ __forceinline__ int swz_index(int i, int j) {
+  // element (row i, column j) of a stage: sub-tile i/16, 128-byte line j, 16-byte
+  // chunk (i%16)/2 XOR (j%8), 8-byte half i%2  (doubles)
+  return (i >> 4) * (S * 16) + j * 16 + ((((i & 15) >> 1) ^ (j & 7)) << 1) + (i & 1);
+}
+
+template <int S, int NST>
+__global__ void __launch_bounds__(S) near_pair_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                      const int4* __restrict__ desc, const int* __restrict__ mirror,
+                                                      long long cnt, const double* __restrict__ xm,
+                                                      double* __restrict__ part) {
+  constexpr int STAGE = S * S + 2 * S;  // doubles; S*S*8 is a multiple of 1024
+  extern __shared__ __align__(1024) double np_smem[];
+  __shared__ __align__(8) unsigned long long bars[NST];
+  const int tid = threadIdx.x;
+  // the swizzle atom needs 1024-byte aligned sub-tiles (offset kept in shared space)
+  double* base = np_smem + (((1024u - (smem_u32(np_smem) & 1023u)) & 1023u) >> 3);
+  if (tid == 0) {
+    for (int q = 0; q < NST; ++q) mbar_init(&bars[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  // desc = {L, first column of the stored block, col.lower (x_sigma), row.lower (x_tau)}
+  auto issue = [&](int st, const int4 d) {
+    double* dst = base + st * STAGE;
+    mbar_expect_tx(&bars[st], static_cast<unsigned>(S * S + 2 * S) * 8u);
+#pragma unroll
+    for (int q = 0; q < S / 16; ++q) {
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+          "[%4];\n" ::"r"(smem_u32(dst + q * S * 16)),
+          "l"(reinterpret_cast<unsigned long long>(&tmap)), "r"(16 * q), "r"(d.y), "r"(smem_u32(&bars[st]))
+          : "memory");
+    }
+    bulk_g2s(dst + S * S, xm + d.z, S * 8u, &bars[st]);
+    bulk_g2s(dst + S * S + S, xm + d.w, S * 8u, &bars[st]);
+  };
+  if (tid == 0)
+    for (int st = 0; st < NST; ++st) {
+      const long long idx = blockIdx.x + static_cast<long long>(st) * gridDim.x;
+      if (idx < cnt) issue(st, desc[idx]);
+    }
+  // per-thread swizzle offsets (see swz_index): row walk (i = tid) and column walk (j = tid)
+  int o1[8], o2[8];
+#pragma unroll
+  for (int b8 = 0; b8 < 8; ++b8) {
+    o1[b8] = (tid >> 4) * (S * 16) + ((((tid & 15) >> 1) ^ b8) << 1) + (tid & 1);
+    o2[b8] = tid * 16 + ((b8 ^ (tid & 7)) << 1);
+  }
+  int st = 0;
+  unsigned ph = 0;
+  for (long long idx = blockIdx.x; idx < cnt; idx += gridDim.x) {
+    // metadata of the block this stage receives next: its loads overlap the folds
+    const long long nidx = idx + static_cast<long long>(NST) * gridDim.x;
+    int4 nd = make_int4(0, 0, 0, 0);
+    if (tid == 0 && nidx < cnt) nd = desc[nidx];
+    const int L = desc[idx].x, M = mirror[idx];
+    mbar_wait(&bars[st], ph);
+    const double* B = base + st * STAGE;
+    const double* xs = B + S * S;
+    const double* xt = xs + S;
+    double y = 0.0, y2 = 0.0;
+    if (M >= 0) {
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        // row walk: element (tid, j); column walk: element (j, tid)
+        y = hadd(y, hmul(B[o1[j & 7] + j * 16], xs[j]));
+        y2 = hadd(y2, hmul(B[(j >> 4) * (S * 16) + o2[(j & 15) >> 1] + (j & 1)], xt[j]));
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < S; ++j) y = hadd(y, hmul(B[o1[j & 7] + j * 16], xs[j]));
+    }
+    part[static_cast<long long>(L) * S + tid] = y;
+    if (M >= 0) part[static_cast<long long>(M) * S + tid] = y2;
+    __syncthreads();  // stage consumed by every thread
+    if (tid == 0 && nidx < cnt) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(st, nd);
+    }
+    if (++st == NST) {
+      st = 0;
+      ph ^= 1u;
+    }
+  }
+}
+
+__global__ void pair_desc_kernel(const int* __restrict__ list, long long cnt, const int* __restrict__ rl,
+                                 const int* __restrict__ cl, const long long* __restrict__ off, int S,
+                                 int4* __restrict__ desc) {
+  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < cnt;
+       q += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int L = list[q];
+    desc[q] = make_int4(L, static_cast<int>(off[L] / S), cl[L], rl[L]);
+  }
+}
+
 struct TmaArgs {
   RowArgs r;
   int D;
   const int* a_tslot;   // aca leaf -> row-cluster slot
+  const double* part;   // symmetric near field: per-dense-leaf products (S each), nullptr: stored blocks
 };
 
 // Item cursor over the dense spans (column chunks of CW) then the aca spans of
@@ -339,7 +476,15 @@ __global__ void __launch_bounds__(S) rows_tma_kernel(TmaArgs A) {
       return;
     }
     const int L = k.L;
-    if (!k.far) {
+    if (!k.far && A.part) {
+      // CW consecutive dense leaves of the span: their S-row partial products (contiguous)
+      const int cnt = min(CW, k.L_end - L);
+      sdesc[st] = 1024 | 512 | cnt;
+      const unsigned bytes = static_cast<unsigned>(S) * cnt * 8u;
+      mbar_expect_tx(&bars[st], bytes);
+      bulk_g2s(sdata[st], A.part + static_cast<long long>(L) * S, bytes, &bars[st]);
+      k.L += cnt;
+    } else if (!k.far) {
       const int nb = __ldg(a.d_n + L);
       const int cnt = min(CW, nb - k.j0);
       const bool last = k.j0 + CW >= nb;
@@ -402,21 +547,25 @@ __global__ void __launch_bounds__(S) rows_tma_kernel(TmaArgs A) {
     const double* dd = sdata[st] + tid;
     const double* da = saux[st];
     // dense: ((0 + a_0 x_0) + a_1 x_1) + ... (dense_blocks.cpp:114); far: ((0 + u_0 t_0) + ...) (aca.cpp:616)
-    if (cnt == CW) {
-      double av[CW], xv[CW];
-#pragma unroll
-      for (int q = 0; q < CW; ++q) {
-        av[q] = dd[q * S];
-        xv[q] = da[q];
-      }
-#pragma unroll
-      for (int q = 0; q < CW; ++q) y = hadd(y, hmul(av[q], xv[q]));
+    if (desc & 1024) {  // symmetric near field: the dense leaves' products, in leaf order (hmatrix.cpp:80-104)
+      for (int q = 0; q < cnt; ++q) z = hadd(z, dd[q * S]);
     } else {
-      for (int q = 0; q < cnt; ++q) y = hadd(y, hmul(dd[q * S], da[q]));
-    }
-    if (desc & 256) {
-      z = hadd(z, y);
-      y = 0.0;
+      if (cnt == CW) {
+        double av[CW], xv[CW];
+#pragma unroll
+        for (int q = 0; q < CW; ++q) {
+          av[q] = dd[q * S];
+          xv[q] = da[q];
+        }
+#pragma unroll
+        for (int q = 0; q < CW; ++q) y = hadd(y, hmul(av[q], xv[q]));
+      } else {
+        for (int q = 0; q < cnt; ++q) y = hadd(y, hmul(dd[q * S], da[q]));
+      }
+      if (desc & 256) {
+        z = hadd(z, y);
+        y = 0.0;
+      }
     }
     __syncthreads();  // stage st consumed by every thread
     if (tid == 0) {
@@ -868,18 +1017,63 @@ static void own_range(const LeafList& l, long long rb, long long re, long long& 
 void store_near_field(HMatrix& h, cudaStream_t s) {
   long long lo, hi;
   own_range(h.dense, h.row_begin, h.row_end, lo, hi);
+  // symmetric storage: regular geometry on the TMA product with every dense leaf S x S
+  h.near_sym = false;
+  const long long S = h.n >> h.dmax_leaf;
+  if (h.tma_rows && std::getenv("HM_NO_SYM") == nullptr) {
+    bool ok = true;
+    for (long long b = lo; b < hi && ok; ++b) ok = h.dense.h_m[b] == S && h.dense.h_n[b] == S;
+    h.near_sym = ok;
+  }
+  // a leaf is stored unless it is the lower half of a pair whose mirror this rank also owns
+  auto stored = [&](long long b) {
+    if (b < lo || b >= hi) return false;
+    if (!h.near_sym) return true;
+    const long long r0 = h.dense.h_rl[b], c0 = h.dense.h_cl[b];
+    return !(r0 > c0 && c0 >= h.row_begin && c0 < h.row_end);
+  };
   std::vector<long long> off(h.dense.count + 1, 0);
-  for (long long b = 0; b < h.dense.count; ++b)
-    off[b + 1] = off[b] + static_cast<long long>(h.dense.h_m[b]) * h.dense.h_n[b];
+  std::vector<int> list;
+  long long run = 0;
+  for (long long b = 0; b < h.dense.count; ++b) {
+    off[b] = run;
+    if (stored(b)) {
+      run += static_cast<long long>(h.dense.h_m[b]) * h.dense.h_n[b];
+      if (h.near_sym) list.push_back(static_cast<int>(b));
+    }
+  }
+  off[h.dense.count] = run;
+  h.S_d_stored = static_cast<double>(run);
   h.dense_off.alloc(off.size(), s);
   HM_CUDA(cudaMemcpyAsync(h.dense_off.get(), off.data(), sizeof(long long) * off.size(), cudaMemcpyHostToDevice, s));
-  const long long total = off[hi] - off[lo];
-  h.dense_vals.alloc(std::max(total, 1ll), s);
-  const unsigned grid = static_cast<unsigned>(std::min<long long>(std::max(hi - lo, 1ll), 148ll * 32));
+  h.dense_vals.alloc(std::max(run, 1ll), s);
+  const int* dlist = nullptr;
+  long long q0 = lo, q1 = hi;
+  if (h.near_sym) {
+    h.n_pairs = static_cast<long long>(list.size());
+    h.pair_leaf.alloc(std::max<size_t>(list.size(), 1), s);
+    h.pair_mirror.alloc(std::max<size_t>(list.size(), 1), s);
+    if (!list.empty())
+      HM_CUDA(cudaMemcpyAsync(h.pair_leaf.get(), list.data(), sizeof(int) * list.size(), cudaMemcpyHostToDevice, s));
+    mirror_kernel<<<grid_for(h.n_pairs, 256, 1 << 16), 256, 0, s>>>(h.pair_leaf.get(), h.n_pairs, h.dense.rl.get(),
+                                                                     h.dense.cl.get(), h.dense.count, h.row_begin,
+                                                                     h.row_end, h.pair_mirror.get());
+    HM_LAUNCH_CHECK();
+    h.part.alloc(std::max(h.dense.count * S, 1ll), s);
+    h.pair_desc.alloc(std::max(h.n_pairs, 1ll), s);
+    pair_desc_kernel<<<grid_for(h.n_pairs, 256, 1 << 16), 256, 0, s>>>(h.pair_leaf.get(), h.n_pairs, h.dense.rl.get(),
+                                                                        h.dense.cl.get(), h.dense_off.get(),
+                                                                        static_cast<int>(S), h.pair_desc.get());
+    HM_LAUNCH_CHECK();
+    dlist = h.pair_leaf.get();
+    q0 = 0;
+    q1 = h.n_pairs;
+  }
+  const unsigned grid = static_cast<unsigned>(std::min<long long>(std::max(q1 - q0, 1ll), 148ll * 32));
 #define HM_STORE(D)                                                                                                   \
   store_dense_kernel<D><<<grid, 256, 0, s>>>(h.coords.get(), h.n, h.d, h.kp, h.dense.rl.get(), h.dense.m.get(),       \
-                                             h.dense.cl.get(), h.dense.n.get(), lo, hi, h.dense_off.get(), off[lo],  \
-                                             h.dense_vals.get())
+                                             h.dense.cl.get(), h.dense.n.get(), q0, q1, h.dense_off.get(), 0,        \
+                                             h.dense_vals.get(), dlist)
   switch (h.d) {
     case 1: HM_STORE(1); break;
     case 2: HM_STORE(2); break;
@@ -888,6 +1082,48 @@ void store_near_field(HMatrix& h, cudaStream_t s) {
     default: HM_STORE(0); break;
   }
 #undef HM_STORE
+  HM_LAUNCH_CHECK();
+}
+
+// TMA tensor map over the stored near field viewed as [columns][S rows] doubles
+static CUtensorMap near_tensor_map(const HMatrix& h, int S) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q{};
+    void* fn = nullptr;
+    HM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) raise(kEcuda, "cuTensorMapEncodeTiled not available");
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  CUtensorMap m;
+  const cuuint64_t cols = static_cast<cuuint64_t>(std::max(h.S_d_stored, static_cast<double>(S)) / S);
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(S), cols};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(S) * 8};
+  const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(S)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, h.dense_vals.get(), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise(kEcuda, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return m;
+}
+
+template <int S>
+void launch_near_pairs(HMatrix& h, cudaStream_t s) {
+  constexpr int NST = 3;
+  const size_t smem = sizeof(double) * static_cast<size_t>(NST) * (S * S + 2 * S) + 1024;
+  HM_CUDA(cudaFuncSetAttribute(near_pair_kernel<S, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+  int occ = 0, sms = 0;
+  HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, near_pair_kernel<S, NST>, S, smem));
+  HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h.device));
+  const long long grid = std::min<long long>(h.n_pairs, static_cast<long long>(std::max(occ, 1)) * sms);
+  const CUtensorMap tm = near_tensor_map(h, S);
+  near_pair_kernel<S, NST><<<static_cast<unsigned>(std::max(grid, 1ll)), S, smem, s>>>(
+      tm, h.pair_desc.get(), h.pair_mirror.get(), h.n_pairs, h.xm.get(), h.part.get());
   HM_LAUNCH_CHECK();
 }
 
@@ -965,6 +1201,12 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
     HM_CUDA(cudaMemcpyAsync(&ub, h.u_off.get() + alo, sizeof(long long), cudaMemcpyDeviceToHost, s));
     HM_CUDA(cudaMemcpyAsync(&vb, h.v_off.get() + alo, sizeof(long long), cudaMemcpyDeviceToHost, s));
     HM_CUDA(cudaStreamSynchronize(s));
+    if (h.near_sym && h.n_pairs > 0) {
+      h.clk.start(kKNearPairs, s);
+      if ((h.n >> h.dmax_leaf) == 64) launch_near_pairs<64>(h, s);
+      else launch_near_pairs<32>(h, s);
+      h.clk.stop(kKNearPairs, s);
+    }
     // aca_order covers [alo, ahi) from the precompute
     h.clk.start(kKLowrankT, s);
     launch_t(h, ahi - alo, vb, s);
@@ -978,6 +1220,7 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
       A.r = a;
       A.D = h.dmax_leaf;
       A.a_tslot = h.aca.tau_slot.get();
+      A.part = h.near_sym ? h.part.get() : nullptr;
       const long long S = h.n >> h.dmax_leaf;
       const unsigned ncl = static_cast<unsigned>((h.row_end - h.row_begin) / S);
       if (S == 64 && h.cfg.k <= 16) rows_tma_kernel<64, 16, 5><<<ncl, 64, 0, s>>>(A);
