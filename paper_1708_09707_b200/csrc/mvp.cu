@@ -276,6 +276,26 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// L2 policies for the bulk streams: the operator (dense blocks, U, V) is read once per
+// product and must not evict the small vectors every leaf re-reads (x segments, t).
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long l2_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                              unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 
 // symmetric near field: mirror of every own stored leaf by binary search in the
 // canonical (row.lower, col.lower) order of equal-depth dense leaves
@@ -333,6 +353,7 @@ __global__ void __launch_bounds__(S) near_pair_kernel(const __grid_constant__ CU
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  const unsigned long long pol_keep = l2_evict_last();
   // desc = {L, first column of the stored block, col.lower (x_sigma), row.lower (x_tau)}
   auto issue = [&](int st, const int4 d) {
     double* dst = base + st * STAGE;
@@ -345,8 +366,8 @@ __global__ void __launch_bounds__(S) near_pair_kernel(const __grid_constant__ CU
           "l"(reinterpret_cast<unsigned long long>(&tmap)), "r"(16 * q), "r"(d.y), "r"(smem_u32(&bars[st]))
           : "memory");
     }
-    bulk_g2s(dst + S * S, xm + d.z, S * 8u, &bars[st]);
-    bulk_g2s(dst + S * S + S, xm + d.w, S * 8u, &bars[st]);
+    bulk_g2s_hint(dst + S * S, xm + d.z, S * 8u, &bars[st], pol_keep);
+    bulk_g2s_hint(dst + S * S + S, xm + d.w, S * 8u, &bars[st], pol_keep);
   };
   if (tid == 0)
     for (int st = 0; st < NST; ++st) {
@@ -433,6 +454,7 @@ __global__ void __launch_bounds__(S) rows_tma_kernel(TmaArgs A) {
   const RowArgs& a = A.r;
   const long long c = static_cast<long long>(blockIdx.x) + a.row_begin / S;
   const int tid = threadIdx.x;
+  const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
 
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
@@ -482,7 +504,7 @@ __global__ void __launch_bounds__(S) rows_tma_kernel(TmaArgs A) {
       sdesc[st] = 1024 | 512 | cnt;
       const unsigned bytes = static_cast<unsigned>(S) * cnt * 8u;
       mbar_expect_tx(&bars[st], bytes);
-      bulk_g2s(sdata[st], A.part + static_cast<long long>(L) * S, bytes, &bars[st]);
+      bulk_g2s_hint(sdata[st], A.part + static_cast<long long>(L) * S, bytes, &bars[st], pol_stream);
       k.L += cnt;
     } else if (!k.far) {
       const int nb = __ldg(a.d_n + L);
@@ -492,9 +514,9 @@ __global__ void __launch_bounds__(S) rows_tma_kernel(TmaArgs A) {
       const unsigned bytes = static_cast<unsigned>(S) * cnt * 8u;
       const unsigned xb = static_cast<unsigned>((cnt + 1) & ~1) * 8u;
       mbar_expect_tx(&bars[st], bytes + xb);
-      bulk_g2s(sdata[st], a.d_vals + (__ldg(a.d_off + L) - a.d_off_base) + static_cast<long long>(k.j0) * S, bytes,
-               &bars[st]);
-      bulk_g2s(saux[st], a.xm + __ldg(a.d_cl + L) + k.j0, xb, &bars[st]);
+      bulk_g2s_hint(sdata[st], a.d_vals + (__ldg(a.d_off + L) - a.d_off_base) + static_cast<long long>(k.j0) * S,
+                    bytes, &bars[st], pol_stream);
+      bulk_g2s_hint(saux[st], a.xm + __ldg(a.d_cl + L) + k.j0, xb, &bars[st], pol_keep);
       if (last) {
         k.j0 = 0;
         ++k.L;
@@ -515,9 +537,10 @@ __global__ void __launch_bounds__(S) rows_tma_kernel(TmaArgs A) {
                      : "memory");
       } else {
         mbar_expect_tx(&bars[st], static_cast<unsigned>(ke2) * (S + 1) * 8u);
-        bulk_g2s(sdata[st], a.U + (__ldg(a.a_uoff + L) - a.a_ubase) + q * a.kmax * S,
-                 static_cast<unsigned>(ke2) * S * 8u, &bars[st]);
-        bulk_g2s(saux[st], a.t + static_cast<long long>(L) * a.kmax, static_cast<unsigned>(ke2) * 8u, &bars[st]);
+        bulk_g2s_hint(sdata[st], a.U + (__ldg(a.a_uoff + L) - a.a_ubase) + q * a.kmax * S,
+                      static_cast<unsigned>(ke2) * S * 8u, &bars[st], pol_stream);
+        bulk_g2s_hint(saux[st], a.t + static_cast<long long>(L) * a.kmax, static_cast<unsigned>(ke2) * 8u, &bars[st],
+                      pol_keep);
       }
       ++k.L;
     }
@@ -662,6 +685,7 @@ __global__ void __launch_bounds__(WARPS * 32) t_fold_kernel(const int* __restric
                                                             const double* __restrict__ xm, int kmax,
                                                             int* __restrict__ counter, double* __restrict__ t) {
   extern __shared__ __align__(128) unsigned char tf_smem[];
+  const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int stage_v = CH * kmax;          // doubles of V per stage
   const int stage_x = CH + 2;             // doubles of x per stage (aligned-down start)
@@ -736,8 +760,8 @@ __global__ void __launch_bounds__(WARPS * 32) t_fold_kernel(const int* __restric
     d[3] = (pj == 0 ? 1 : 0) | (pj + cnt == pn ? 2 : 0) | (pke << 2);
     const unsigned vb = static_cast<unsigned>(cnt) * kmax * 8u;
     mbar_expect_tx(&bars[st], vb + xcnt * 8u);
-    bulk_g2s(dv, V + pvo + static_cast<long long>(pj) * kmax, vb, &bars[st]);
-    bulk_g2s(dx, xm + xa, xcnt * 8u, &bars[st]);
+    bulk_g2s_hint(dv, V + pvo + static_cast<long long>(pj) * kmax, vb, &bars[st], pol_stream);
+    bulk_g2s_hint(dx, xm + xa, xcnt * 8u, &bars[st], pol_keep);
     pj += cnt;
     if (pj == pn) pb = -1;
   };
@@ -807,6 +831,7 @@ __global__ void __launch_bounds__(WARPS * 32) t_pair_kernel(const int* __restric
   constexpr int SX = CH + 2;       // doubles of one leaf's x chunk
   constexpr int STAGE = 2 * SV + 2 * SX;
   extern __shared__ __align__(128) unsigned char tp_smem[];
+  const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = lane >> 4, l = lane & 15;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(tp_smem) + warp * NST;
@@ -882,10 +907,11 @@ __global__ void __launch_bounds__(WARPS * 32) t_pair_kernel(const int* __restric
       mbar_expect_tx(&bars[st], bytes);
       for (int q = 0; q < nl; ++q) {
         if (pke[q] == 0) continue;
-        bulk_g2s(dv + q * SV, V + pvo[q] + static_cast<long long>(pj) * KM, static_cast<unsigned>(cnt) * KM * 8u,
-                 &bars[st]);
+        bulk_g2s_hint(dv + q * SV, V + pvo[q] + static_cast<long long>(pj) * KM, static_cast<unsigned>(cnt) * KM * 8u,
+                      &bars[st], pol_stream);
         const long long xa = (pcl[q] + pj) & ~1ll;
-        bulk_g2s(dv + 2 * SV + q * SX, xm + xa, static_cast<unsigned>((xoff[q] + cnt + 1) & ~1) * 8u, &bars[st]);
+        bulk_g2s_hint(dv + 2 * SV + q * SX, xm + xa, static_cast<unsigned>((xoff[q] + cnt + 1) & ~1) * 8u, &bars[st],
+                      pol_keep);
       }
     }
     pj += cnt;
@@ -1113,7 +1139,7 @@ static CUtensorMap near_tensor_map(const HMatrix& h, int S) {
 
 template <int S>
 void launch_near_pairs(HMatrix& h, cudaStream_t s) {
-  constexpr int NST = 3;
+  constexpr int NST = 2;  // 2 x 34 KB per CTA -> 3 CTAs (6 blocks in flight) per SM
   const size_t smem = sizeof(double) * static_cast<size_t>(NST) * (S * S + 2 * S) + 1024;
   HM_CUDA(cudaFuncSetAttribute(near_pair_kernel<S, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
@@ -1201,16 +1227,28 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
     HM_CUDA(cudaMemcpyAsync(&ub, h.u_off.get() + alo, sizeof(long long), cudaMemcpyDeviceToHost, s));
     HM_CUDA(cudaMemcpyAsync(&vb, h.v_off.get() + alo, sizeof(long long), cudaMemcpyDeviceToHost, s));
     HM_CUDA(cudaStreamSynchronize(s));
+    // the near-field pair kernel and the V^T x fold are independent HBM streams: run
+    // them concurrently (auxiliary stream) so each fills the other's ramp and tail
+    // (serial while the per-kernel event clock is on, so each kernel's time is its own)
+    const bool near_par = h.near_sym && h.n_pairs > 0 && !h.clk.on && std::getenv("HM_SERIAL_NEAR") == nullptr;
     if (h.near_sym && h.n_pairs > 0) {
-      h.clk.start(kKNearPairs, s);
-      if ((h.n >> h.dmax_leaf) == 64) launch_near_pairs<64>(h, s);
-      else launch_near_pairs<32>(h, s);
-      h.clk.stop(kKNearPairs, s);
+      cudaStream_t sn = s;
+      if (near_par) {
+        HM_CUDA(cudaEventRecord(h.ev_fork, s));
+        HM_CUDA(cudaStreamWaitEvent(h.aux, h.ev_fork, 0));
+        sn = h.aux;
+      }
+      h.clk.start(kKNearPairs, sn);
+      if ((h.n >> h.dmax_leaf) == 64) launch_near_pairs<64>(h, sn);
+      else launch_near_pairs<32>(h, sn);
+      h.clk.stop(kKNearPairs, sn);
+      if (near_par) HM_CUDA(cudaEventRecord(h.ev_join, h.aux));
     }
     // aca_order covers [alo, ahi) from the precompute
     h.clk.start(kKLowrankT, s);
     launch_t(h, ahi - alo, vb, s);
     h.clk.stop(kKLowrankT, s);
+    if (near_par) HM_CUDA(cudaStreamWaitEvent(s, h.ev_join, 0));
     a.a_ubase = ub;
     a.a_lo = alo;
     a.a_hi = ahi;

@@ -1,16 +1,14 @@
-# GPU round: tests, bench (C2), launch list, ncu captures.  Usage: bash tools/gpu_round.sh [quick|full|ncu]
+# Full GPU round: smoke, GPU suite, C2 bench (+CPU baseline), reference arm, ncu launch list and
+# full captures of the product kernels (exported to CSV on the box).  Usage: bash tools/gpu_round.sh [tag]
 set -x
-MODE=${1:-full}
+TAG=${1:-r1}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -5
-if [ "$MODE" != "ncu" ]; then
-  timeout 900 python bench.py --steps 30 --warmup 3 --cpu-baseline $([ "$MODE" = full ] && echo 1 || echo 0) > gpurun_out/bench.json 2> gpurun_out/bench.err
-  tail -c 4000 gpurun_out/bench.json; tail -3 gpurun_out/bench.err
-fi
-if [ "$MODE" != "quick" ]; then
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'rows_kernel|lowrank|gather|scatter' -c 60 --csv --log-file gpurun_out/launches.csv python bench.py --steps 4 --warmup 1 --cpu-baseline 0 > /dev/null 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'rows_kernel' -s 1 -c 1 -o gpurun_out/prof_rows python bench.py --n 262144 --steps 2 --warmup 1 --cpu-baseline 0 > gpurun_out/ncu_rows.log 2>&1; tail -3 gpurun_out/ncu_rows.log
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'lowrank_t' -s 2 -c 2 -o gpurun_out/prof_t python bench.py --n 262144 --steps 2 --warmup 1 --cpu-baseline 0 > gpurun_out/ncu_t.log 2>&1; tail -3 gpurun_out/ncu_t.log
-fi
-ls -la gpurun_out
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; tail -1 gpurun_out/smoke_$TAG.log
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu_$TAG.log 2>&1; tail -3 gpurun_out/pytest_gpu_$TAG.log
+timeout 900 python bench.py --steps 30 --warmup 3 > gpurun_out/bench_c2_$TAG.json 2> gpurun_out/bench_c2_$TAG.err; tail -c 600 gpurun_out/bench_c2_$TAG.json
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$TAG.json 2>&1; tail -c 300 gpurun_out/bench_ref_$TAG.json
+timeout 900 ncu -f --metrics gpu__time_duration.sum --clock-control none -k regex:'rows_tma|t_pair|near_pair|gather_x|scatter_z' -c 40 --csv --log-file gpurun_out/launches_c2_$TAG.csv python bench.py --steps 2 --warmup 1 --cpu-baseline 0 > /dev/null 2>&1
+timeout 1500 ncu -f --set full --clock-control none --import-source on -k regex:'rows_tma|t_pair|near_pair' -s 3 -c 3 -o /tmp/prod_$TAG python bench.py --steps 2 --warmup 1 --cpu-baseline 0 > gpurun_out/ncu_prod_$TAG.log 2>&1; tail -2 gpurun_out/ncu_prod_$TAG.log
+ncu -i /tmp/prod_$TAG.ncu-rep --page details --csv > gpurun_out/prod_${TAG}_details.csv 2>/dev/null
+ncu -i /tmp/prod_$TAG.ncu-rep --page raw --csv --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum > gpurun_out/prod_${TAG}_raw.csv 2>/dev/null
+ls -la gpurun_out | tail -20
