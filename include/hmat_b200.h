@@ -111,6 +111,22 @@ hm_status hm_mvp_local(hm_handle* h, const double* x, double* z_slice);
 /* hmat::cg_solve(HMatrix, kernel, b, SolveConfig) -- solver.hpp:27-28 (host vectors). */
 hm_status hm_cg_solve(hm_handle* h, const double* b, double sigma2, double tol, int64_t max_iter, double* x,
                       int64_t* iterations, double* relative_residual);
+/* ---- multiple right-hand sides (BASELINE config 5) ----
+ * X, Z: n x nrhs column-major (column r at X + r*n), original ordering.  One pass over
+ * the operator serves up to 16 vectors (larger nrhs runs in passes of 16).
+ * flags = HM_MULTI_EXACT: column r is bitwise equal to hm_mvp of X[:, r].
+ * flags = HM_MULTI_DMMA : recompute-mode near field contracted on the FP64 tensor cores
+ *                         (nrhs 8 or 16 per pass); per-leaf sums in a different order. */
+#define HM_MULTI_EXACT 0
+#define HM_MULTI_DMMA 1
+hm_status hm_mvp_multi(hm_handle* h, const double* X, double* Z, int64_t nrhs, int32_t flags);
+hm_status hm_mvp_multi_device(hm_handle* h, const double* X_dev, double* Z_dev, int64_t nrhs, int32_t flags,
+                              void* stream);
+/* nrhs independent hmat::cg_solve runs in lock-step on multi-RHS products (B, X: n x nrhs);
+ * iterations / relative_residual: one entry per right-hand side. */
+hm_status hm_cg_solve_multi(hm_handle* h, const double* B, int64_t nrhs, double sigma2, double tol, int64_t max_iter,
+                            int32_t flags, double* X, int64_t* iterations, double* relative_residual);
+
 /* hmat::relative_error (hmatrix.hpp:63) -- exact product on the device, no N limit. */
 hm_status hm_relative_error(hm_handle* h, const double* x, double* out);
 /* exact dense product z = A x (oracle.cpp:24-55 semantics, device), original ordering */

@@ -115,6 +115,12 @@ _sig("hm_profile_begin", C.c_int, [_p])
 _sig("hm_profile_end", C.c_int, [_p, _p, _p])
 _sig("hm_log_port_host", None, [_i64, _p, _p])
 _sig("hm_log_port_device", C.c_int, [_i64, _p, _p])
+_sig("hm_mvp_multi", C.c_int, [_p, _p, _p, _i64, _i32])
+_sig("hm_mvp_multi_device", C.c_int, [_p, _p, _p, _i64, _i32, _p])
+_sig("hm_cg_solve_multi", C.c_int, [_p, _p, _i64, _d, _d, _i64, _i32, _p, _p, _p])
+
+HM_MULTI_EXACT = 0
+HM_MULTI_DMMA = 1
 
 EXPORTED_SYMBOLS = [
     "hm_last_error", "hm_config_default", "hm_device_count", "hm_setup", "hm_setup_device", "hm_destroy",
@@ -122,6 +128,7 @@ EXPORTED_SYMBOLS = [
     "hm_dense_mvp", "hm_get_stats", "hm_get_timings", "hm_get_points", "hm_get_codes", "hm_get_leaves",
     "hm_get_aca", "hm_morton_codes", "hm_morton_order", "hm_aca_dense", "hm_eval_kernel", "hm_exp_port_host",
     "hm_exp_port_device", "hm_log_port_host", "hm_log_port_device", "hm_profile_begin", "hm_profile_end",
+    "hm_mvp_multi", "hm_mvp_multi_device", "hm_cg_solve_multi",
 ]
 
 KERNEL_IDS = ["gather_x", "lowrank_t", "rows", "scatter_z", "aca", "rows_far", "allgather", "near_pairs"]
@@ -250,6 +257,23 @@ class HMatrix:
         if timings is not None:
             timings.total_ms = t.mvp_ms
         return z
+
+    def mvp_multi(self, X, dmma: bool = False) -> np.ndarray:
+        """Z[:, r] = H X[:, r] for every column of X (n x nrhs), one operator pass per 16
+        columns.  dmma=False: each column bitwise equal to mvp(X[:, r]); dmma=True: the
+        recompute-mode near field on the FP64 tensor cores (nrhs 8 or 16 per pass)."""
+        X = np.asarray(X, dtype=np.float64)
+        if X.ndim != 2 or X.shape[0] != self.n:
+            raise InvalidArgument(HM_EINVAL, "mvp_multi: X must be n x nrhs")
+        Xc = np.ascontiguousarray(X.T)  # rhs-major = column-major n x nrhs
+        Z = np.empty_like(Xc)
+        _check(_lib.hm_mvp_multi(self._h, _ptr(Xc), _ptr(Z), Xc.shape[0], HM_MULTI_DMMA if dmma else HM_MULTI_EXACT))
+        return Z.T
+
+    def mvp_multi_device(self, x_ptr: int, z_ptr: int, nrhs: int, dmma: bool = False, stream: int = 0) -> None:
+        """Device arrays, column-major n x nrhs (original ordering)."""
+        _check(_lib.hm_mvp_multi_device(self._h, C.c_void_p(x_ptr), C.c_void_p(z_ptr), int(nrhs),
+                                        HM_MULTI_DMMA if dmma else HM_MULTI_EXACT, C.c_void_p(stream or None)))
 
     def mvp_device(self, x_ptr: int, z_ptr: int, stream: int = 0) -> None:
         """Device pointers (original ordering) on a CUDA stream handle (0 = the handle's stream)."""
@@ -392,6 +416,22 @@ def cg_solve(h: HMatrix, kernel: Optional[KernelFunction], b, config: SolveConfi
     _check(_lib.hm_cg_solve(h._h, _ptr(b), float(config.sigma2), float(config.tol), int(config.max_iter), _ptr(x),
                             C.byref(it), C.byref(rr)))
     return SolveResult(x, int(it.value), float(rr.value))
+
+
+def cg_solve_multi(h: HMatrix, B, config: SolveConfig = SolveConfig(), dmma: bool = False):
+    """nrhs independent cg_solve runs (solver.cpp:19-73) on multi-RHS products.
+    B: n x nrhs.  Returns (X n x nrhs, iterations[nrhs], relative_residual[nrhs])."""
+    B = np.asarray(B, dtype=np.float64)
+    if B.ndim != 2 or B.shape[0] != h.n:
+        raise InvalidArgument(HM_EINVAL, "cg_solve_multi: B must be n x nrhs")
+    Bc = np.ascontiguousarray(B.T)
+    R = Bc.shape[0]
+    X = np.empty_like(Bc)
+    it = np.zeros(R, dtype=np.int64)
+    rr = np.zeros(R)
+    _check(_lib.hm_cg_solve_multi(h._h, _ptr(Bc), R, float(config.sigma2), float(config.tol), int(config.max_iter),
+                                  HM_MULTI_DMMA if dmma else HM_MULTI_EXACT, _ptr(X), _ptr(it), _ptr(rr)))
+    return X.T, it, rr
 
 
 def morton_codes(coords) -> np.ndarray:

@@ -1,6 +1,7 @@
 // hm_api.cu -- the C ABI (include/hmat_b200.h): host orchestration in C++,
 // exceptions mapped to hm_status at the boundary.
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -292,6 +293,39 @@ void product(hm_handle* H, const double* x_dev, double* z_dev, cudaStream_t s) {
   h.clk.stop(kKScatter, s);
 }
 
+// R right-hand sides per pass (multi.cu); X, Z rhs-major device arrays (original order)
+void product_multi(hm_handle* H, const double* X_dev, double* Z_dev, int R, int flags, cudaStream_t s) {
+  HMatrix& h = H->h;
+  const long long n = h.n;
+  ensure_multi(h, R, s);
+  gather_multi(h, X_dev, n, R, s);
+  mvp_multi_morton(h, R, flags, s);
+  if (h.cfg.world > 1) {
+    if (!H->comm) raise(kEnccl, "world > 1 but no NCCL communicator attached (hm_attach_nccl)");
+    const std::vector<long long>& bounds = H->rank_bounds;
+    const NcclApi& nc = NcclApi::get();
+    if (nc.GroupStart() != ncclSuccess) raise(kEnccl, "ncclGroupStart");
+    for (int r = 0; r < R; ++r)
+      for (int g = 0; g < h.cfg.world; ++g) {
+        double* p = h.zmR.get() + static_cast<long long>(r) * n + bounds[g];
+        if (nc.Broadcast(p, p, static_cast<size_t>(bounds[g + 1] - bounds[g]), ncclDouble, g, H->comm, s) !=
+            ncclSuccess)
+          raise(kEnccl, "ncclBroadcast of a y slice failed");
+      }
+    if (nc.GroupEnd() != ncclSuccess) raise(kEnccl, "ncclGroupEnd");
+  }
+  scatter_multi(h, Z_dev, n, R, s);
+}
+
+// nrhs in passes of at most 16
+void product_multi_all(hm_handle* H, const double* X_dev, double* Z_dev, long long nrhs, int flags, cudaStream_t s) {
+  const long long n = H->h.n;
+  for (long long r0 = 0; r0 < nrhs; r0 += 16) {
+    const int R = static_cast<int>(std::min<long long>(16, nrhs - r0));
+    product_multi(H, X_dev + r0 * n, Z_dev + r0 * n, R, flags, s);
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -537,6 +571,128 @@ hm_status hm_cg_solve(hm_handle* H, const double* b, double sigma2, double tol, 
       diff_sq += dd * dd;
     }
     *rel_res = std::sqrt(diff_sq) / b_norm;
+  });
+}
+
+hm_status hm_mvp_multi(hm_handle* H, const double* X, double* Z, int64_t nrhs, int32_t flags) {
+  return guarded([&] {
+    if (!H || !X || !Z) raise(kEinval, "mvp_multi: null argument");
+    if (nrhs < 1) raise(kEinval, "mvp_multi: nrhs must be >= 1");
+    std::lock_guard<std::mutex> lock(H->mu);
+    HMatrix& h = H->h;
+    HM_CUDA(cudaSetDevice(h.device));
+    cudaStream_t s = h.stream;
+    const size_t tot = static_cast<size_t>(h.n) * nrhs;
+    if (h.xinR.size() < tot) h.xinR.alloc(tot, s);
+    if (h.zoutR.size() < tot) h.zoutR.alloc(tot, s);
+    HM_CUDA(cudaMemcpyAsync(h.xinR.get(), X, sizeof(double) * tot, cudaMemcpyHostToDevice, s));
+    product_multi_all(H, h.xinR.get(), h.zoutR.get(), nrhs, flags, s);
+    HM_CUDA(cudaMemcpyAsync(Z, h.zoutR.get(), sizeof(double) * tot, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+hm_status hm_mvp_multi_device(hm_handle* H, const double* X_dev, double* Z_dev, int64_t nrhs, int32_t flags,
+                              void* stream) {
+  return guarded([&] {
+    if (!H || !X_dev || !Z_dev) raise(kEinval, "mvp_multi: null argument");
+    if (nrhs < 1) raise(kEinval, "mvp_multi: nrhs must be >= 1");
+    std::lock_guard<std::mutex> lock(H->mu);
+    HM_CUDA(cudaSetDevice(H->h.device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : H->h.stream;
+    product_multi_all(H, X_dev, Z_dev, nrhs, flags, s);
+  });
+}
+
+// nrhs independent cg_solve runs (solver.cpp:19-73) in lock-step: one multi-RHS product
+// per iteration for all vectors; each keeps its own scalars and stopping rule, so with
+// flags = 0 every column follows exactly the single-RHS iteration.
+hm_status hm_cg_solve_multi(hm_handle* H, const double* B, int64_t nrhs, double sigma2, double tol, int64_t max_iter,
+                            int32_t flags, double* X, int64_t* iterations, double* rel_res) {
+  return guarded([&] {
+    if (!H || !B || !X || !iterations || !rel_res) raise(kEinval, "cg_solve_multi: null argument");
+    if (nrhs < 1) raise(kEinval, "cg_solve_multi: nrhs must be >= 1");
+    if (tol <= 0.0) raise(kEinval, "cg_solve: tol must be > 0");
+    if (max_iter < 1) raise(kEinval, "cg_solve: max_iter must be >= 1");
+    if (sigma2 < 0.0) raise(kEinval, "cg_solve: sigma2 must be >= 0");
+    std::lock_guard<std::mutex> lock(H->mu);
+    HMatrix& h = H->h;
+    HM_CUDA(cudaSetDevice(h.device));
+    cudaStream_t s = h.stream;
+    const long long n = h.n, R = nrhs;
+    DevBuf<double> db, dx, dr, dp, dap, part, alpha;
+    db.alloc(n * R, s);
+    dx.alloc(n * R, s);
+    dr.alloc(n * R, s);
+    dp.alloc(n * R, s);
+    dap.alloc(n * R, s);
+    alpha.alloc(R, s);
+    HM_CUDA(cudaMemcpyAsync(db.get(), B, sizeof(double) * n * R, cudaMemcpyHostToDevice, s));
+    dx.zero(s);
+    HM_CUDA(cudaMemcpyAsync(dr.get(), db.get(), sizeof(double) * n * R, cudaMemcpyDeviceToDevice, s));
+    HM_CUDA(cudaMemcpyAsync(dp.get(), db.get(), sizeof(double) * n * R, cudaMemcpyDeviceToDevice, s));
+    std::vector<double> bn(R), rs(R);
+    std::vector<char> active(R, 1);
+    for (long long r = 0; r < R; ++r) {
+      iterations[r] = 0;
+      rel_res[r] = 0.0;
+      bn[r] = std::sqrt(device_dot(db.get() + r * n, db.get() + r * n, n, part, s));
+      if (bn[r] == 0.0) active[r] = 0;
+      rs[r] = device_dot(dr.get() + r * n, dr.get() + r * n, n, part, s);
+    }
+    const unsigned grid = grid_for(n, 256, 1 << 16);
+    bool any = std::any_of(active.begin(), active.end(), [](char c) { return c != 0; });
+    for (long long iter = 1; iter <= max_iter && any; ++iter) {
+      product_multi_all(H, dp.get(), dap.get(), R, flags, s);
+      any = false;
+      for (long long r = 0; r < R; ++r) {
+        if (!active[r]) continue;
+        double* pr = dp.get() + r * n;
+        double* apr = dap.get() + r * n;
+        axpy_sigma_kernel<<<grid, 256, 0, s>>>(apr, pr, sigma2, n);
+        HM_LAUNCH_CHECK();
+        const double a = rs[r] / device_dot(pr, apr, n, part, s);
+        HM_CUDA(cudaMemcpyAsync(alpha.get() + r, &a, sizeof(double), cudaMemcpyHostToDevice, s));
+        cg_update_kernel<<<grid, 256, 0, s>>>(dx.get() + r * n, dr.get() + r * n, pr, apr, alpha.get() + r, n);
+        HM_LAUNCH_CHECK();
+        const double rs_next = device_dot(dr.get() + r * n, dr.get() + r * n, n, part, s);
+        if (!std::isfinite(rs_next) || !std::isfinite(a))
+          raise(kEnonfinite, "cg_solve: non-finite value at iteration " + std::to_string(iter) + " (rhs " +
+                                 std::to_string(r) + ")");
+        iterations[r] = iter;
+        if (std::sqrt(rs_next) <= tol * bn[r]) {
+          active[r] = 0;
+          continue;
+        }
+        const double beta = rs_next / rs[r];
+        cg_dir_kernel<<<grid, 256, 0, s>>>(pr, dr.get() + r * n, beta, n);
+        HM_LAUNCH_CHECK();
+        rs[r] = rs_next;
+        any = true;
+      }
+    }
+    // true residuals of the returned iterates (solver.cpp:64-71)
+    product_multi_all(H, dx.get(), dap.get(), R, flags, s);
+    for (long long r = 0; r < R; ++r) {
+      axpy_sigma_kernel<<<grid, 256, 0, s>>>(dap.get() + r * n, dx.get() + r * n, sigma2, n);
+      HM_LAUNCH_CHECK();
+    }
+    std::vector<double> ax(n * R);
+    HM_CUDA(cudaMemcpyAsync(ax.data(), dap.get(), sizeof(double) * n * R, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaMemcpyAsync(X, dx.get(), sizeof(double) * n * R, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+    for (long long r = 0; r < R; ++r) {
+      if (bn[r] == 0.0) {
+        std::memset(X + r * n, 0, sizeof(double) * n);
+        continue;
+      }
+      double diff_sq = 0.0;
+      for (long long i = 0; i < n; ++i) {
+        const double dd = B[r * n + i] - ax[r * n + i];
+        diff_sq += dd * dd;
+      }
+      rel_res[r] = std::sqrt(diff_sq) / bn[r];
+    }
   });
 }
 

@@ -127,6 +127,9 @@ struct HMatrix {
 
   // product workspaces
   DevBuf<double> xm, zm, xin, zout;
+  // multi-RHS workspaces (multi.cu): rhs-major vectors, chunk-relative t, symmetric partials
+  DevBuf<double> xmR, zmR, tR, partR, xinR, zoutR;
+  DevBuf<long long> dmma_tiles;
   DevBuf<int> counter;
 
   // algorithmic sizes
@@ -145,6 +148,11 @@ void build_hmatrix(HMatrix& h, const double* coords_dev);
 void mvp_device(HMatrix& h, const double* x_dev, double* z_dev, cudaStream_t s);
 // Morton-ordered product into h.zm (rows [row_begin,row_end)), x already in h.xm.
 void mvp_morton(HMatrix& h, cudaStream_t s);
+// R right-hand sides (multi.cu): h.xmR -> h.zmR; flags bit 0: DMMA near field
+void ensure_multi(HMatrix& h, int R, cudaStream_t s);
+void gather_multi(HMatrix& h, const double* X, long long ldx, int R, cudaStream_t s);
+void scatter_multi(HMatrix& h, double* Z, long long ldz, int R, cudaStream_t s);
+void mvp_multi_morton(HMatrix& h, int R, int flags, cudaStream_t s);
 
 // components
 void morton_codes_device(const double* coords, long long n, int d, unsigned long long* codes, cudaStream_t s);
