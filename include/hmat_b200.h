@@ -127,6 +127,10 @@ hm_status hm_mvp_multi_device(hm_handle* h, const double* X_dev, double* Z_dev, 
 hm_status hm_cg_solve_multi(hm_handle* h, const double* B, int64_t nrhs, double sigma2, double tol, int64_t max_iter,
                             int32_t flags, double* X, int64_t* iterations, double* relative_residual);
 
+/* hmat::dump_leaves_csv (tree.hpp:94, tree.cpp:197-205): every leaf of the block tree in
+ * canonical order, "row_lower,row_upper,col_lower,col_upper,admissible" (HM_ELOGIC when
+ * the file cannot be written, the reference's runtime_error). */
+hm_status hm_dump_leaves_csv(hm_handle* h, const char* path);
 /* hmat::relative_error (hmatrix.hpp:63) -- exact product on the device, no N limit. */
 hm_status hm_relative_error(hm_handle* h, const double* x, double* out);
 /* exact dense product z = A x (oracle.cpp:24-55 semantics, device), original ordering */

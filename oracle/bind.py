@@ -283,5 +283,20 @@ class Reference(_Checker):
         return out
 
 
+REF_DUMP_CSV = os.path.join(HERE, "_ref", "ref_dump_csv")
+
+
+def reference_leaf_csv(coords, c_leaf, eta, path):
+    """The reference's own dump_leaves_csv (tree.cpp:197-205) after its setup(), run in a
+    separate process (oracle/ref_dump_csv.cpp)."""
+    import subprocess
+    import tempfile
+    c = np.ascontiguousarray(coords, dtype=np.float64)
+    d, n = c.shape
+    with tempfile.NamedTemporaryFile(suffix=".bin") as f:
+        c.tofile(f.name)
+        subprocess.run([REF_DUMP_CSV, str(n), str(d), str(c_leaf), repr(float(eta)), f.name, str(path)], check=True)
+
+
 def available(kind: str) -> bool:
     return os.path.exists(REF_SO if kind == "ref" else ORACLE_SO)

@@ -10,6 +10,7 @@
 // The reference worker pool races with more than one thread (SURVEY.md F1,
 // parallel.cpp:33-92), so the constructor below pins HMAT_THREADS=1 unless the
 // caller set it explicitly.
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstdlib>

@@ -116,6 +116,7 @@ _sig("hm_profile_end", C.c_int, [_p, _p, _p])
 _sig("hm_log_port_host", None, [_i64, _p, _p])
 _sig("hm_log_port_device", C.c_int, [_i64, _p, _p])
 _sig("hm_mvp_multi", C.c_int, [_p, _p, _p, _i64, _i32])
+_sig("hm_dump_leaves_csv", C.c_int, [_p, C.c_char_p])
 _sig("hm_mvp_multi_device", C.c_int, [_p, _p, _p, _i64, _i32, _p])
 _sig("hm_cg_solve_multi", C.c_int, [_p, _p, _i64, _d, _d, _i64, _i32, _p, _p, _p])
 
@@ -128,7 +129,7 @@ EXPORTED_SYMBOLS = [
     "hm_dense_mvp", "hm_get_stats", "hm_get_timings", "hm_get_points", "hm_get_codes", "hm_get_leaves",
     "hm_get_aca", "hm_morton_codes", "hm_morton_order", "hm_aca_dense", "hm_eval_kernel", "hm_exp_port_host",
     "hm_exp_port_device", "hm_log_port_host", "hm_log_port_device", "hm_profile_begin", "hm_profile_end",
-    "hm_mvp_multi", "hm_mvp_multi_device", "hm_cg_solve_multi",
+    "hm_mvp_multi", "hm_mvp_multi_device", "hm_cg_solve_multi", "hm_dump_leaves_csv",
 ]
 
 KERNEL_IDS = ["gather_x", "lowrank_t", "rows", "scatter_z", "aca", "rows_far", "allgather", "near_pairs"]
@@ -274,6 +275,10 @@ class HMatrix:
         """Device arrays, column-major n x nrhs (original ordering)."""
         _check(_lib.hm_mvp_multi_device(self._h, C.c_void_p(x_ptr), C.c_void_p(z_ptr), int(nrhs),
                                         HM_MULTI_DMMA if dmma else HM_MULTI_EXACT, C.c_void_p(stream or None)))
+
+    def dump_leaves_csv(self, path: str) -> None:
+        """dump_leaves_csv (tree.cpp:197-205): all leaves, canonical order, reference format."""
+        _check(_lib.hm_dump_leaves_csv(self._h, os.fsencode(path)))
 
     def mvp_device(self, x_ptr: int, z_ptr: int, stream: int = 0) -> None:
         """Device pointers (original ordering) on a CUDA stream handle (0 = the handle's stream)."""

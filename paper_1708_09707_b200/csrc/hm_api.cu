@@ -4,10 +4,12 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/hmat_b200.h"
@@ -693,6 +695,33 @@ hm_status hm_cg_solve_multi(hm_handle* H, const double* B, int64_t nrhs, double 
       }
       rel_res[r] = std::sqrt(diff_sq) / bn[r];
     }
+  });
+}
+
+// dump_leaves_csv (tree.cpp:197-205): every leaf in canonical order (tree.cpp:189-194),
+// the dense and admissible lists merged back, with the reference's header and format
+hm_status hm_dump_leaves_csv(hm_handle* H, const char* path) {
+  return guarded([&] {
+    if (!H || !path) raise(kEinval, "dump_leaves_csv: null argument");
+    std::lock_guard<std::mutex> lock(H->mu);
+    const HMatrix& h = H->h;
+    FILE* f = std::fopen(path, "w");
+    if (!f) raise(kElogic, std::string("dump_leaves_csv: cannot open ") + path);
+    std::fputs("row_lower,row_upper,col_lower,col_upper,admissible\n", f);
+    const LeafList& D = h.dense;
+    const LeafList& A = h.aca;
+    long long i = 0, j = 0;
+    auto key = [](const LeafList& l, long long q) {
+      return std::make_tuple(l.h_rl[q], l.h_rl[q] + l.h_m[q], l.h_cl[q], l.h_cl[q] + l.h_n[q]);
+    };
+    while (i < D.count || j < A.count) {
+      const bool take_d = j >= A.count || (i < D.count && key(D, i) < key(A, j));
+      const LeafList& l = take_d ? D : A;
+      const long long q = take_d ? i++ : j++;
+      std::fprintf(f, "%d,%d,%d,%d,%d\n", l.h_rl[q], l.h_rl[q] + l.h_m[q], l.h_cl[q], l.h_cl[q] + l.h_n[q],
+                   take_d ? 0 : 1);
+    }
+    if (std::fclose(f) != 0) raise(kElogic, std::string("dump_leaves_csv: write failed ") + path);
   });
 }
 

@@ -201,3 +201,24 @@ def test_bench_config_parity_row_sampled(gpu, oracle):
     zo = o.mvp_rows(x, ranges)
     for lo, hi in ranges:
         assert np.array_equal(bits(zm[lo:hi]), bits(zo[lo:hi]))
+
+
+@pytest.mark.parametrize("n,d,c_leaf", [(64, 2, 8), (3001, 2, 48), (4096, 3, 64)])
+def test_leaf_csv_dump_matches_reference(gpu, n, d, c_leaf, tmp_path):
+    """dump_leaves_csv (tree.cpp:197-205): same file, byte for byte, as the reference's own
+    function on the same points (oracle/_ref), header and canonical leaf order included."""
+    from oracle.bind import available, reference_leaf_csv
+    P = uniform_points(n, d, 79)
+    h = gpu.setup(P, gpu.KernelFunction(), gpu.HmatrixConfig(c_leaf=c_leaf))
+    ours = tmp_path / "ours.csv"
+    h.dump_leaves_csv(str(ours))
+    lines = ours.read_text().splitlines()
+    assert lines[0] == "row_lower,row_upper,col_lower,col_upper,admissible"
+    st = h.stats()
+    assert len(lines) - 1 == st["n_dense"] + st["n_aca"]
+    if available("ref"):
+        ref = tmp_path / "ref.csv"
+        reference_leaf_csv(P, c_leaf, 1.5, ref)
+        assert ours.read_bytes() == ref.read_bytes()
+    with pytest.raises(gpu.HmError):
+        h.dump_leaves_csv(str(tmp_path / "no_such_dir" / "x.csv"))

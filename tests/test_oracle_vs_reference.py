@@ -100,3 +100,23 @@ def test_f3_epsilon_inert_when_eta_above_one(oracle):
     a = oracle.setup(P, c_leaf=64, k=16, epsilon=1e-6).mvp(x)
     b = oracle.setup(P, c_leaf=64, k=16).mvp(x)
     assert np.array_equal(bits(a), bits(b))
+
+
+@pytest.mark.parametrize("cfg", CONFIGS[:4], ids=[str(c) for c in CONFIGS[:4]])
+def test_reference_leaf_csv_is_the_merged_canonical_list(oracle, reference, cfg, tmp_path):
+    """The reference's dump_leaves_csv (tree.cpp:197-205) lists exactly the oracle's dense and
+    admissible leaves merged in canonical order -- the contract hm_dump_leaves_csv follows."""
+    n, d, c_leaf, kern, k, eta = cfg
+    P = uniform_points(n, d, 1234 + n)
+    from oracle.bind import reference_leaf_csv
+    path = tmp_path / "leaves.csv"
+    reference_leaf_csv(P, c_leaf, eta, path)
+    lines = path.read_text().splitlines()
+    assert lines[0] == "row_lower,row_upper,col_lower,col_upper,admissible"
+    got = np.array([[int(v) for v in ln.split(",")] for ln in lines[1:]], dtype=np.int64).reshape(-1, 5)
+    ho = oracle.setup(P, kernel=kern, c_leaf=c_leaf, k=k, eta=eta)
+    rows = np.concatenate([ho.leaves(0, boxes=False).rows, ho.leaves(1, boxes=False).rows])
+    flags = np.concatenate([np.zeros(ho.count(0), np.int64), np.ones(ho.count(1), np.int64)])
+    order = np.lexsort((rows[:, 3], rows[:, 2], rows[:, 1], rows[:, 0]))
+    want = np.column_stack([rows[order], flags[order]])
+    assert np.array_equal(got, want)
