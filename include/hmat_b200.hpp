@@ -228,6 +228,41 @@ inline SolveResult cg_solve(const HMatrix& h, const KernelFunction& /*kernel*/, 
   return r;
 }
 
+// ---- B200 extensions (no reference counterpart) ----
+// Z[:, r] = H X[:, r]; X, Z column-major n x nrhs.  dmma = false: every column bitwise
+// equal to mvp(X[:, r]); dmma = true: recompute near field on the FP64 tensor cores.
+inline std::vector<double> mvp_multi(const HMatrix& h, std::span<const double> X, std::int64_t nrhs,
+                                     bool dmma = false) {
+  if (nrhs < 1 || static_cast<std::int64_t>(X.size()) != h.size() * nrhs)
+    throw std::invalid_argument("mvp_multi: X must hold n * nrhs values");
+  std::vector<double> Z(X.size());
+  check(hm_mvp_multi(h.handle(), X.data(), Z.data(), nrhs, dmma ? HM_MULTI_DMMA : HM_MULTI_EXACT));
+  return Z;
+}
+struct SolveResultMulti {
+  std::vector<double> x;  // n x nrhs, column-major
+  std::vector<std::int64_t> iterations;
+  std::vector<double> relative_residual;
+};
+// nrhs independent cg_solve runs (solver.cpp:19-73) on multi-RHS products
+inline SolveResultMulti cg_solve_multi(const HMatrix& h, std::span<const double> B, std::int64_t nrhs,
+                                       const SolveConfig& config, bool dmma = false) {
+  if (nrhs < 1 || static_cast<std::int64_t>(B.size()) != h.size() * nrhs)
+    throw std::invalid_argument("cg_solve_multi: B must hold n * nrhs values");
+  SolveResultMulti r;
+  r.x.resize(B.size());
+  r.iterations.resize(static_cast<std::size_t>(nrhs));
+  r.relative_residual.resize(static_cast<std::size_t>(nrhs));
+  check(hm_cg_solve_multi(h.handle(), B.data(), nrhs, config.sigma2, config.tol, config.max_iter,
+                          dmma ? HM_MULTI_DMMA : HM_MULTI_EXACT, r.x.data(),
+                          reinterpret_cast<int64_t*>(r.iterations.data()), r.relative_residual.data()));
+  return r;
+}
+// tree.hpp:94 dump_leaves_csv, for the leaves of a set-up H-matrix (canonical order)
+inline void dump_leaves_csv(const HMatrix& h, const std::string& path) {
+  check(hm_dump_leaves_csv(h.handle(), path.c_str()));
+}
+
 // morton.hpp:23-26
 inline std::vector<std::uint64_t> compute_morton_codes(const PointSet& points) {
   const std::vector<double> flat = flatten(points);

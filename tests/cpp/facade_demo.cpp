@@ -33,6 +33,15 @@ int main() {
   hmat::SolveConfig sc;
   sc.sigma2 = 1.0;
   const hmat::SolveResult r = hmat::cg_solve(h, kernel, x, sc);
+  // B200 extensions: 8 right-hand sides in one operator pass, column 0 == the single product
+  std::vector<double> X(static_cast<std::size_t>(points.count) * 8);
+  for (std::size_t q = 0; q < X.size(); ++q) X[q] = 1.0 + 0.001 * static_cast<double>(q % 97);
+  for (std::int64_t i = 0; i < points.count; ++i) X[i] = 1.0;
+  const std::vector<double> Z = hmat::mvp_multi(h, X, 8);
+  for (std::int64_t i = 0; i < points.count; ++i)
+    if (Z[i] != z[i]) return 2;
+  hmat::dump_leaves_csv(h, "facade_leaves.csv");
+  std::remove("facade_leaves.csv");
   double nz = 0.0;
   for (double v : z) nz += v * v;
   std::printf("facade ok: N=%lld dense=%zu aca=%zu |z|=%.12g e_rel=%.3e cg_iters=%lld relres=%.3e\n",
