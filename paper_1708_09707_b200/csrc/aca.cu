@@ -818,7 +818,10 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
     for (int r = 0; r < kmax; ++r) {
       int acc_w = -1;
       while (next < n) {
-        const int wcols = min(W, n - next);
+        // speculation depth: while no column was rejected, at most kmax - r more can be
+        // accepted (smooth blocks, d >= 3: no noise floor), so do not evaluate past them
+        const int lim = rejections ? W : max(kmax - r, 1);
+        const int wcols = max(filled, min(min(W, lim), n - next));
         ev_col += static_cast<unsigned long long>(wcols - filled) * m;
         // fill: fresh window columns, entry then the reference chain over l < r
         for (int co = filled; co < wcols; ++co) {
@@ -1133,7 +1136,10 @@ __global__ void __launch_bounds__(kBigThreads) aca_big_kernel(AcaJob J, KernelEn
     for (int r = 0; r < kmax; ++r) {
       int acc_w = -1;
       while (next < n) {
-        const int wcols = min(W, n - next);
+        // speculation depth: while no column was rejected, at most kmax - r more can be
+        // accepted (smooth blocks, d >= 3: no noise floor), so do not evaluate past them
+        const int lim = rejections ? W : max(kmax - r, 1);
+        const int wcols = max(filled, min(min(W, lim), n - next));
         ev_col += static_cast<unsigned long long>(wcols - filled) * m;
         // fill: per row pair, u of the two rows into registers once, then every fresh column
         for (int i0 = t; i0 < m; i0 += 2 * TT) {

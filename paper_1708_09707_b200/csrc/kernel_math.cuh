@@ -38,6 +38,17 @@ HM_HD double hm_div(double a, double b) {
 #endif
 }
 
+// Loop-invariant quotients/products of the series (bessel_k1_tables.inc): the device
+// loop does one division per term; values are bitwise what the loop computes.
+struct K1Tables {
+  double inv1[64], inv2[64], den[64];
+};
+#ifdef __CUDACC__
+static __constant__ K1Tables kK1Dev =
+#include "bessel_k1_tables.inc"
+    ;
+#endif
+
 // core.cpp:28-47
 HM_HD double bessel_k1_series(double x) {
   const double kEulerGamma = 0.57721566490153286060651209008240243;
@@ -50,11 +61,19 @@ HM_HD double bessel_k1_series(double x) {
   for (int j = 0; j < 64; ++j) {
     sum_i1 = hadd(sum_i1, term);
     sum_k = hadd(sum_k, hmul(hadd(psi_a, psi_b), term));
+#ifdef __CUDA_ARCH__
+    const double next = hm_div(hmul(term, q), kK1Dev.den[j]);
+    if (next < hmul(1e-19, hadd(sum_i1, 1.0))) break;
+    term = next;
+    psi_a = hadd(psi_a, kK1Dev.inv1[j]);
+    psi_b = hadd(psi_b, kK1Dev.inv2[j]);
+#else
     const double next = hm_div(hmul(term, q), hmul(j + 1.0, j + 2.0));
     if (next < hmul(1e-19, hadd(sum_i1, 1.0))) break;
     term = next;
     psi_a = hadd(psi_a, hm_div(1.0, j + 1.0));
     psi_b = hadd(psi_b, hm_div(1.0, j + 2.0));
+#endif
   }
   const double i1 = hmul(hmul(0.5, x), sum_i1);
   return hsub(hadd(hm_div(1.0, x), hmul(hm_log(hmul(0.5, x)), i1)), hmul(hmul(0.25, x), sum_k));

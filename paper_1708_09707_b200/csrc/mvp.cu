@@ -1281,7 +1281,8 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
   size_t free_b = 0, total_b = 0;
   HM_CUDA(cudaMemGetInfo(&free_b, &total_b));
   long long budget = h.cfg.aca_chunk_rows > 0 ? h.cfg.aca_chunk_rows * kmax * 16
-                                              : std::min<long long>(static_cast<long long>(free_b / 4), 8ll << 30);
+                                              : std::max<long long>(static_cast<long long>(h.U.bytes() + h.V.bytes()),
+                                                                std::min<long long>(static_cast<long long>(free_b / 2), 96ll << 30));
   budget = std::max(budget, 1ll << 20);
   long long c0 = alo;
   while (c0 < ahi) {
