@@ -222,3 +222,30 @@ def test_leaf_csv_dump_matches_reference(gpu, n, d, c_leaf, tmp_path):
         assert ours.read_bytes() == ref.read_bytes()
     with pytest.raises(gpu.HmError):
         h.dump_leaves_csv(str(tmp_path / "no_such_dir" / "x.csv"))
+
+
+@pytest.mark.parametrize("cfg", [
+    # BASELINE configs[2]: N=2^22, [0,1]^3, Matern (nu = 1), matrix-free near field
+    dict(n=1 << 22, d=3, kernel="matern", kind=1),
+    # BASELINE configs[3] geometry: N=2^24, [0,1]^3, Gaussian, matrix-free (one GPU)
+    dict(n=1 << 24, d=3, kernel="gaussian", kind=0),
+], ids=["C3_2^22_d3_matern", "C4_2^24_d3_gaussian"])
+def test_full_size_configs_row_sampled(gpu, oracle, cfg):
+    """BASELINE configs 3 and 4 at their full N, in the reference's default recompute mode
+    (ACA inside every product): sampled row clusters of the GPU product are bitwise equal
+    to the reference order (row-sampled oracle)."""
+    n, d = cfg["n"], cfg["d"]
+    P = uniform_points(n, d, 42)
+    x = symmetric(43, n)
+    h = gpu.setup(P, gpu.KernelFunction(cfg["kernel"]), gpu.HmatrixConfig(c_leaf=64, k=16))
+    z = h.mvp(x)
+    o = oracle.setup(P, kernel=cfg["kind"], c_leaf=64, k=16)
+    _, perm = o.points()
+    _, hperm = h.points()
+    assert np.array_equal(perm, hperm)
+    zm = z[perm]
+    S = n >> h.stats()["dmax_leaf"]
+    ranges = [(0, S), (n // 3 // S * S, n // 3 // S * S + S), (n - S, n)]
+    zo = oracle_rows = o.mvp_rows(x, ranges)
+    for lo, hi in ranges:
+        assert np.array_equal(bits(zm[lo:hi]), bits(oracle_rows[lo:hi])), (lo, np.max(np.abs(zm[lo:hi] - zo[lo:hi])))

@@ -102,3 +102,20 @@ def test_block_cg_follows_single_rhs_cg(gpu, oracle):
     Xd, itd, rrd = gpu.cg_solve_multi(h, B[:, :2].repeat(4, axis=1), cfg, dmma=True)
     assert np.all(rrd <= 1e-7)
     assert np.linalg.norm(Xd[:, 0] - X[:, 0]) / np.linalg.norm(X[:, 0]) <= 1e-9
+
+
+def test_config5_full_size_multi_rhs(gpu):
+    """BASELINE configs[4] geometry at full size: N = 2^22 uniform points in [0,1]^4, matrix-free
+    (recompute) near and far field, 16 right-hand sides per pass.  Size-independent
+    properties: exact-mode columns bitwise equal to single-RHS products, DMMA columns within
+    1e-12 of them."""
+    n, d, R = 1 << 22, 4, 16
+    P = uniform_points(n, d, 42)
+    h = gpu.setup(P, gpu.KernelFunction(), gpu.HmatrixConfig(c_leaf=64, k=16))
+    X = rhs(n, R)
+    Ze = h.mvp_multi(X)
+    for r in (0, R - 1):
+        assert np.array_equal(bits(Ze[:, r]), bits(h.mvp(X[:, r])))
+    Zd = h.mvp_multi(X, dmma=True)
+    rel = np.linalg.norm(Zd - Ze, axis=0) / np.linalg.norm(Ze, axis=0)
+    assert np.all(rel <= 1e-12), rel.max()
