@@ -249,3 +249,30 @@ def test_full_size_configs_row_sampled(gpu, oracle, cfg):
     zo = oracle_rows = o.mvp_rows(x, ranges)
     for lo, hi in ranges:
         assert np.array_equal(bits(zm[lo:hi]), bits(oracle_rows[lo:hi])), (lo, np.max(np.abs(zm[lo:hi] - zo[lo:hi])))
+
+
+def test_cli_compatible_csv_outputs(gpu, oracle, tmp_path):
+    """tools/hmat_csv.py writes the reference CLI's CSV formats (hmat_cli.cpp:117-255):
+    headers, one row per phase, and --dump-leaves as dense queue then aca queue."""
+    import subprocess
+    import sys as _sys
+    from paper_1708_09707_b200.inputs import halton_points
+    repo = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+    tool = [_sys.executable, f"{repo}/tools/hmat_csv.py"]
+    out = tmp_path / "bench.csv"
+    leaves = tmp_path / "leaves.csv"
+    subprocess.run(tool + ["--command", "mvp-bench", "--n", "4096", "--c-leaf", "64", "--trials", "2", "--precompute",
+                           "--out", str(out), "--dump-leaves", str(leaves)], check=True)
+    rows = out.read_text().splitlines()
+    assert rows[0] == "phase,n,d,k,eta,c_leaf,time_ms_mean,time_ms_std"
+    assert [r.split(",")[0] for r in rows[1:]] == ["setup", "mvp", "mvp_dense", "mvp_aca"]
+    assert all(r.split(",")[1:6] == ["4096", "2", "16", "1.5", "64"] for r in rows[1:])
+    o = oracle.setup(halton_points(4096, 2), c_leaf=64, k=16)
+    want = np.concatenate([np.column_stack([o.leaves(w, boxes=False).rows, np.full(o.count(w), w)]) for w in (0, 1)])
+    got = np.loadtxt(leaves, delimiter=",", skiprows=1, dtype=np.int64)
+    assert np.array_equal(got, want)
+    conv = subprocess.run(tool + ["--command", "convergence", "--n", "2048", "--c-leaf", "64", "--trials", "1"],
+                          check=True, capture_output=True, text=True).stdout.splitlines()
+    assert conv[0] == "kernel,d,k,e_rel_mean" and len(conv) == 9
+    errs = [float(r.split(",")[3]) for r in conv[1:5]]
+    assert errs == sorted(errs, reverse=True) and errs[-1] < 1e-6
