@@ -1377,15 +1377,16 @@ __global__ void class_key_kernel(const int* __restrict__ m, const int* __restric
   }
 }
 
-__global__ void size_key_kernel(const int* __restrict__ m, const int* __restrict__ nn, long long begin, long long cnt,
-                                unsigned long long* __restrict__ keys, unsigned* __restrict__ vals) {
+__global__ void size_key_kernel(const int* __restrict__ m, const int* __restrict__ nn, const int* __restrict__ cl,
+                                long long begin, long long cnt, unsigned long long* __restrict__ keys,
+                                unsigned* __restrict__ vals) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < cnt;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long b = begin + i;
-    // n descending, then m descending: largest first, and the n >= 2048 blocks of the
-    // low-rank apply form a prefix
-    keys[i] = ((~static_cast<unsigned long long>(nn[b]) & 0xffffffffull) << 32) |
-              (~static_cast<unsigned long long>(m[b]) & 0xffffffffull);
+    // long leaves (n >= 4096, whose folds are the critical path) first, largest first;
+    // the rest in leaf order, i.e. V in address order (a sequential HBM stream)
+    const unsigned long long big = nn[b] >= 4096 ? static_cast<unsigned long long>(nn[b]) : 0ull;
+    keys[i] = ((~big & 0xffffffffull) << 32) | static_cast<unsigned long long>(b - begin);
     vals[i] = static_cast<unsigned>(b);
   }
 }
@@ -1404,7 +1405,8 @@ void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStrea
   DevBuf<unsigned long long> keys;
   keys.alloc(cnt, s);
   h.aca_order.alloc(cnt, s);
-  size_key_kernel<<<grid_for(cnt, 256, 1 << 16), 256, 0, s>>>(h.aca.m.get(), h.aca.n.get(), leaf_begin, cnt,
+  size_key_kernel<<<grid_for(cnt, 256, 1 << 16), 256, 0, s>>>(h.aca.m.get(), h.aca.n.get(), h.aca.cl.get(), leaf_begin,
+                                                               cnt,
                                                                keys.get(), reinterpret_cast<unsigned*>(h.aca_order.get()));
   HM_LAUNCH_CHECK();
   radix_sort_pairs(keys.get(), reinterpret_cast<unsigned*>(h.aca_order.get()), cnt, s);

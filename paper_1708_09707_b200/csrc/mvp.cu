@@ -886,10 +886,14 @@ __global__ void __launch_bounds__(WARPS * 32) t_pair_kernel(const int* __restric
     int xoff[2] = {0, 0};
     const int nl = pair ? 2 : 1;
     for (int q = 0; q < nl; ++q) bytes += pke[q] > 0 ? static_cast<unsigned>(cnt) * KM * 8u : 0u;
+    // leaves of a pair with the same column cluster (the queue is column-ordered within
+    // a size) share one x segment
+    const bool xshare = pair && pke[0] > 0 && pke[1] > 0 && pcl[0] == pcl[1];
     for (int q = 0; q < nl; ++q) {
       if (pke[q] == 0) continue;
       const long long xs = pcl[q] + pj, xa = xs & ~1ll;
       xoff[q] = static_cast<int>(xs - xa);
+      if (q == 1 && xshare) continue;
       bytes += static_cast<unsigned>((xoff[q] + cnt + 1) & ~1) * 8u;
     }
     d[0] = pb[0];
@@ -897,7 +901,7 @@ __global__ void __launch_bounds__(WARPS * 32) t_pair_kernel(const int* __restric
     d[2] = cnt;
     d[3] = xoff[0];
     d[4] = xoff[1];
-    d[5] = (pj == 0 ? 1 : 0) | (pj + cnt == pn ? 2 : 0);
+    d[5] = (pj == 0 ? 1 : 0) | (pj + cnt == pn ? 2 : 0) | (xshare ? 4 : 0);
     d[6] = pke[0];
     d[7] = pair ? pke[1] : 0;
     if (bytes == 0) {
@@ -909,6 +913,7 @@ __global__ void __launch_bounds__(WARPS * 32) t_pair_kernel(const int* __restric
         if (pke[q] == 0) continue;
         bulk_g2s_hint(dv + q * SV, V + pvo[q] + static_cast<long long>(pj) * KM, static_cast<unsigned>(cnt) * KM * 8u,
                       &bars[st], pol_stream);
+        if (q == 1 && xshare) continue;
         const long long xa = (pcl[q] + pj) & ~1ll;
         bulk_g2s_hint(dv + 2 * SV + q * SX, xm + xa, static_cast<unsigned>((xoff[q] + cnt + 1) & ~1) * 8u, &bars[st],
                       pol_keep);
@@ -945,7 +950,8 @@ __global__ void __launch_bounds__(WARPS * 32) t_pair_kernel(const int* __restric
     const int cnt = d[2], flags = d[5];
     const int ke = half ? d[7] : d[6];
     const double* dv = sv + static_cast<long long>(st) * STAGE + half * SV + l;
-    const double* dx = sv + static_cast<long long>(st) * STAGE + 2 * SV + half * SX + (half ? d[4] : d[3]);
+    const int xh = (flags & 4) ? 0 : half;  // shared x segment: both halves read slot 0
+    const double* dx = sv + static_cast<long long>(st) * STAGE + 2 * SV + xh * SX + (half ? d[4] : d[3]);
     if (b >= 0 && l < ke) {
       int q = 0;
       if (flags & 1) {
