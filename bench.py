@@ -116,8 +116,16 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- reference arm
 def reference_sample(args, steps: int, warmup: int, workers: int = 0):
     """Run oracle/refbench.py workers (one single-threaded process per core)."""
-    ncores = os.cpu_count() or 1
-    workers = workers or max(1, min(ncores, 16))
+    ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    if not workers:
+        # every usable core, bounded by host memory: one reference setup per process
+        # (~4 GB peak at N = 2^20, d = 2; more at larger N)
+        try:
+            avail_gb = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE") / 2**30
+        except (ValueError, OSError):
+            avail_gb = 64.0
+        per_gb = 4.0 * max(1.0, args.n / float(1 << 20)) * (1.0 + 0.5 * max(0, args.d - 2))
+        workers = max(1, min(ncores, int(avail_gb * 0.7 / per_gb)))
     # leaf-level row clusters spread evenly over [0, N)
     depth = 0
     while ((args.n - 1) >> depth) + 1 > args.c_leaf:

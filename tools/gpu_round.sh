@@ -2,7 +2,7 @@
 # full captures of the product kernels (exported to CSV on the box).  Usage: bash tools/gpu_round.sh [tag]
 set -x
 TAG=${1:-r1}
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader; nproc; free -g | head -2; lscpu | grep "Model name"
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; tail -1 gpurun_out/smoke_$TAG.log
 timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu_$TAG.log 2>&1; tail -3 gpurun_out/pytest_gpu_$TAG.log
 timeout 900 python bench.py --steps 30 --warmup 3 > gpurun_out/bench_c2_$TAG.json 2> gpurun_out/bench_c2_$TAG.err; tail -c 600 gpurun_out/bench_c2_$TAG.json
