@@ -22,6 +22,8 @@
 // FMA contraction), so u/v and the pivots are bitwise the reference's.  The only
 // order-sensitive quantity, norm2, is summed in parallel with a rigorous error
 // bound; decisions inside the bound fall back to the reference's sequential fold.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -1320,6 +1322,398 @@ __global__ void __launch_bounds__(kBigThreads) aca_big_kernel(AcaJob J, KernelEn
   }
 }
 
+// ---------------------------------------------------------------------------
+// Cluster kernel (1024 < max(m, n) <= 512 * CL): a THREAD-BLOCK CLUSTER of CL CTAs
+// (256 threads each) factorises one block.  CTA c of the cluster owns rows
+// [512c, 512c + 512) with u_l right-aligned in registers (exactly the window kernel's
+// thread mapping) and keeps its rows of the W-column window in its own shared memory.
+// Per-column partial norms, the pivot argmax, the exact folds and the pivot row's u_l
+// travel through distributed shared memory (mapa / ld.shared::cluster via
+// cluster.map_shared_rank); every CTA combines the CL partials in rank order, so all
+// CTAs take identical decisions and the whole factorisation is bitwise the reference's.
+// v_l lives in the interleaved V factor (written by the row pass, made visible to the
+// cluster by the release/acquire cluster barrier).
+template <int DIM, int KIND, int KC, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
+    aca_cluster_kernel(AcaJob J, KernelEntry<DIM, KIND> E) {
+  namespace cg = cooperative_groups;
+  constexpr int TT = 256, RPL = 2, NCAP = TT * RPL, W = 16, PS = NCAP + 1, G = TT / W;  // G = 16
+  constexpr int YD = DIM > 0 ? DIM : 1;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cr = static_cast<int>(cluster.block_rank());
+  extern __shared__ double smem[];
+  double* s_win = smem;                       // W x PS (own rows)
+  double* s_up = s_win + W * PS;              // KC: u_l[p] (copied from the owner)
+  double* s_csum = s_up + KC;                 // W: this CTA's partial norm per column
+  int* s_cnz = reinterpret_cast<int*>(s_csum + W);      // W ints
+  double* s_wsum = s_csum + W + W / 2;        // 8 warps x 2 (sum pieces for G=16 groups)
+  double* s_rbv = s_wsum + 16;                // 8 warps (argmax)
+  int* s_rbi = reinterpret_cast<int*>(s_rbv + 8);       // 8 ints
+  double* s_cbv = s_rbv + 12;                 // [0] CTA argmax value, [1] (int) index
+  int* s_state = reinterpret_cast<int*>(s_cbv + 2);     // W ints
+  unsigned char* s_used = reinterpret_cast<unsigned char*>(s_cbv + 2 + W / 2);  // NCAP bytes
+  double* s_misc = s_cbv + 2 + W / 2 + NCAP / 8;  // [0] job [1] scale [2] verdict [3] pivot value
+  double* s_tot = s_misc + 8;                     // W: combined norm per window column
+  double* s_scr = s_tot + W;                      // NCAP: re-evaluated first column (exact scale2)
+  const int t = threadIdx.x, lane = t & 31, wib = t >> 5;
+  const double kEps0sq = 1e-14 * 1e-14;
+  const int kmax = J.kmax;
+  auto rem = [&](double* p, int rank) -> const double* { return cluster.map_shared_rank(p, rank); };
+
+  for (;;) {
+    if (cr == 0 && t == 0) s_misc[0] = static_cast<double>(atomicAdd(J.counter, 1));
+    for (int i = t; i < NCAP; i += TT) s_used[i] = 0;
+    cluster.sync();
+    const long long job = static_cast<long long>(*rem(s_misc, 0));
+    cluster.sync();  // everyone has read the job before rank 0 may overwrite it
+    if (job >= J.njobs) return;
+    const int b = J.order[job];
+    const int rl = J.rl[b], m = J.m[b], cl = J.cl[b], n = J.nn[b];
+    double* U = J.U + (J.u_off[b] - J.u_base);
+    double* V = J.V + (J.v_off[b] - J.v_base);
+    const int tsh = J.tile_shift;
+    auto uix = [&](int l, int i) -> long long {
+      if (tsh < 0) return static_cast<long long>(l) * m + i;
+      return ((static_cast<long long>(i >> tsh) * kmax + l) << tsh) + (i & ((1 << tsh) - 1));
+    };
+    const int row0 = cr * NCAP;  // first block row of this CTA
+    double y[RPL][YD];
+    bool rv[RPL];
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      const int i = row0 + t + q * TT;
+      rv[q] = i < m;
+      if constexpr (DIM > 0) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) y[q][a] = rv[q] ? __ldg(E.coords + a * E.n + rl + i) : 0.0;
+      }
+    }
+    auto entry = [&](int q, long long colpt) -> double {
+      if constexpr (DIM > 0) {
+        return E.eval(y[q], colpt);
+      } else {
+        double yy[20];
+        E.load(rl + row0 + t + q * TT, yy);
+        return E.eval(yy, colpt);
+      }
+    };
+    double uR[RPL][KC];
+#pragma unroll
+    for (int q = 0; q < RPL; ++q)
+#pragma unroll
+      for (int j = 0; j < KC; ++j) uR[q][j] = 0.0;
+    int next = 0, filled = 0, k_eff = 0;
+    unsigned long long rejections = 0, ev_col = 0, ev_row = 0;
+    double scale = -1.0, s_lo = 0.0, s_hi = 0.0;  // scale2: exact (scale_exact) or bracket
+    bool have_scale = false, scale_exact = false;
+    int c0col = 0;
+    const double gm = static_cast<double>(m) * 1.2e-16;
+    // exact left fold of a window column over ALL rows (rank order, then row order)
+    auto exact_fold = [&](int slot) -> double {
+      double f = 0.0;
+      bool first = true;
+      for (int c = 0; c < CL; ++c) {
+        const double* w = rem(s_win, c) + slot * PS;
+        const int rows = min(NCAP, m - c * NCAP);
+        for (int i = 0; i < rows; ++i) {
+          const double a = w[i];
+          f = first ? hmul(a, a) : hadd(f, hmul(a, a));
+          first = false;
+        }
+      }
+      return f;
+    };
+
+    for (int r = 0; r < kmax; ++r) {
+      int acc_w = -1;
+      while (next < n) {
+        const int lim = rejections ? W : max(kmax - r, 1);
+        const int wcols = max(filled, min(min(W, lim), n - next));
+        ev_col += static_cast<unsigned long long>(wcols - filled) * m;
+        for (int co = filled; co < wcols; ++co) {
+          const int col = next + co;
+          double* dst = s_win + (col % W) * PS;
+          double a0 = rv[0] ? entry(0, cl + col) : 0.0;
+          double a1 = rv[1] ? entry(1, cl + col) : 0.0;
+          Chain<KC>::run2(a0, a1, uR[0], uR[1], r, V + static_cast<long long>(col) * kmax + (r - KC), 1);
+          if (rv[0]) dst[t] = a0;
+          if (rv[1]) dst[t + TT] = a1;
+        }
+        filled = wcols;
+        __syncthreads();
+        // this CTA's partial norm / nonzero flag per window column (G = 16 threads each)
+        {
+          const int w = t / G, g = t % G;
+          double sum = 0.0;
+          int nz = 0;
+          if (w < wcols) {
+            const double* src = s_win + ((next + w) % W) * PS;
+            const int rows = min(NCAP, m - row0);
+            for (int i = g; i < rows; i += G) {
+              const double a = src[i];
+              sum = hadd(sum, hmul(a, a));
+              nz |= (!s_used[i] && fabs(a) > 0.0) ? 1 : 0;
+            }
+          }
+#pragma unroll
+          for (int o = G / 2; o; o >>= 1) {
+            sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+            nz |= __shfl_xor_sync(0xffffffffu, nz, o);
+          }
+          if (g == 0) {
+            s_csum[w] = sum;
+            s_cnz[w] = nz;
+          }
+        }
+        cluster.sync();
+        // identical decision in every CTA: partials combined in rank order.  scale2 is
+        // known exactly only on demand (see scale_exact): until then the test uses the
+        // bracket [s_lo, s_hi] of the parallel sum, which contains the exact left fold.
+        if (t < W) {
+          const int w = t;
+          int st = 0;
+          double sum = 0.0;
+          if (w < wcols) {
+            double ps[CL];
+            int pn[CL];
+#pragma unroll
+            for (int c = 0; c < CL; ++c) {  // all remote loads issued before the fold
+              ps[c] = *rem(s_csum + w, c);
+              pn[c] = cluster.map_shared_rank(s_cnz, c)[w];
+            }
+            int nz = 0;
+            sum = ps[0];
+#pragma unroll
+            for (int c = 0; c < CL; ++c) {
+              if (c) sum = hadd(sum, ps[c]);
+              nz |= pn[c];
+            }
+            if (nz) {
+              if (!have_scale) {
+                st = 1;
+              } else {
+                const double Tlo = hmul(kEps0sq, scale_exact ? scale : s_lo);
+                const double Thi = hmul(kEps0sq, scale_exact ? scale : s_hi);
+                const double lo = hmul(sum, 1.0 - 4.0 * gm), hi = hmul(sum, 1.0 + 4.0 * gm);
+                st = lo > Thi ? 1 : (hi <= Tlo ? 0 : 2);
+              }
+            }
+          }
+          s_state[w] = st;
+          s_tot[w] = sum;
+        }
+        __syncthreads();
+        for (int w = 0; w < wcols; ++w) {
+          int st = s_state[w];
+          if (st == 2) {  // the reference's sequential left folds (aca.cpp:373-374, 491)
+            if (!scale_exact) {
+              // the first accepted column is A(:, c0col) (no cross subtracted yet):
+              // re-evaluate it (bitwise the same entries) and fold it over all rows
+#pragma unroll
+              for (int q = 0; q < RPL; ++q)
+                if (rv[q]) s_scr[t + q * TT] = entry(q, cl + c0col);
+              cluster.sync();
+              if (t == 0) {
+                double f = 0.0;
+                bool first = true;
+                for (int c = 0; c < CL; ++c) {
+                  const double* w2 = rem(s_scr, c);
+                  const int rows = min(NCAP, m - c * NCAP);
+                  for (int i = 0; i < rows; ++i) {
+                    f = first ? hmul(w2[i], w2[i]) : hadd(f, hmul(w2[i], w2[i]));
+                    first = false;
+                  }
+                }
+                s_misc[1] = f;
+              }
+              cluster.sync();
+              scale = s_misc[1];
+              scale_exact = true;
+            }
+            if (t == 0) s_misc[2] = exact_fold((next + w) % W) > hmul(kEps0sq, scale) ? 1.0 : 0.0;
+            __syncthreads();
+            st = s_misc[2] != 0.0 ? 1 : 0;
+          }
+          if (st == 1) {
+            acc_w = w;
+            break;
+          }
+        }
+        if (!have_scale && acc_w >= 0) {
+          // first cross: bracket of scale2 from the parallel norm of the accepted column
+          const double sp = s_tot[acc_w];
+          s_lo = hmul(sp, 1.0 - 4.0 * gm);
+          s_hi = hmul(sp, 1.0 + 4.0 * gm);
+          c0col = next + acc_w;
+          have_scale = true;
+        }
+        cluster.sync();  // partials / windows read by every CTA before they change
+        const int consumed = acc_w >= 0 ? acc_w + 1 : wcols;
+        rejections += static_cast<unsigned long long>(acc_w >= 0 ? acc_w : wcols);
+        next += consumed;
+        filled = acc_w >= 0 ? wcols - consumed : 0;
+        if (acc_w >= 0) break;
+      }
+      if (acc_w < 0) break;  // no usable column left (aca.cpp:442-443)
+      const int cstar = next - 1;
+      const int aslot = cstar % W;
+      const double* acol = s_win + aslot * PS;
+
+      // pivot row: argmax over unused rows, first (global) index wins
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        const int il = t + q * TT;
+        if (rv[q] && !s_used[il]) {
+          const double av = fabs(acol[il]);
+          if (av > bv) {
+            bv = av;
+            bi = row0 + il;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        argmax_combine(bv, bi, ov, oi);
+      }
+      if (lane == 0) {
+        s_rbv[wib] = bv;
+        s_rbi[wib] = bi;
+      }
+      __syncthreads();
+      if (t == 0) {
+        double cbv = s_rbv[0];
+        int cbi = s_rbi[0];
+        for (int g = 1; g < TT / 32; ++g) argmax_combine(cbv, cbi, s_rbv[g], s_rbi[g]);
+        s_cbv[0] = cbv;
+        reinterpret_cast<int*>(s_cbv + 1)[0] = cbi;
+      }
+      cluster.sync();
+      int p;
+      {
+        double gbv = -1.0;
+        int gbi = 0x7fffffff;
+        double cv[CL];
+        int ci[CL];
+#pragma unroll
+        for (int c = 0; c < CL; ++c) {
+          const double* rc = rem(s_cbv, c);
+          cv[c] = rc[0];
+          ci[c] = reinterpret_cast<const int*>(rc + 1)[0];
+        }
+#pragma unroll
+        for (int c = 0; c < CL; ++c) argmax_combine(gbv, gbi, cv[c], ci[c]);
+        p = gbi;
+      }
+      const int po = p / NCAP, pl = p - po * NCAP, pt = pl % TT, pq = pl / TT;
+      if (cr == po && t == pt) {
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+          if (q == pq) {
+            s_misc[3] = acol[pl];
+#pragma unroll
+            for (int j = 0; j < KC; ++j)
+              if (j >= KC - r) s_up[j - (KC - r)] = uR[q][j];
+          }
+        }
+      }
+      cluster.sync();
+      // the owner's u_l[p] and pivot value into every CTA
+      if (cr != po) {
+        const double* ru = rem(s_up, po);
+        for (int l = t; l < r; l += TT) s_up[l] = ru[l];
+        if (t == 0) s_misc[3] = *rem(s_misc + 3, po);
+      }
+      __syncthreads();
+      const double pivot_val = s_misc[3];
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        const double nu = rv[q] ? __ddiv_rn(acol[t + q * TT], pivot_val) : 0.0;
+#pragma unroll
+        for (int j = 0; j + 1 < KC; ++j) uR[q][j] = uR[q][j + 1];
+        uR[q][KC - 1] = nu;
+      }
+      // v_r = A(p,:) - sum_l u_l[p] v_l (aca.cpp:474-481), columns split over the cluster
+      ev_row += n;
+      {
+        double yp[DIM > 0 ? DIM : 20];
+        E.load(rl + p, yp);
+        double uP[KC];
+#pragma unroll
+        for (int j = 0; j < KC; ++j) uP[j] = j >= KC - r ? s_up[j - (KC - r)] : 0.0;
+        for (int j = cr * TT + t; j < n; j += CL * TT)
+          V[static_cast<long long>(j) * kmax + r] =
+              Chain<KC>::run(E.eval(yp, cl + j), uP, r, V + static_cast<long long>(j) * kmax + (r - KC), 1);
+      }
+      cluster.sync();  // v_r visible to the whole cluster (release / acquire)
+      if (cr == po && t == pt) s_used[pl] = 1;
+      for (int co = 0; co < filled; ++co) {
+        const int col = next + co;
+        const double vr = V[static_cast<long long>(col) * kmax + r];
+        double* dst = s_win + (col % W) * PS;
+#pragma unroll
+        for (int q = 0; q < RPL; ++q)
+          if (rv[q]) dst[t + q * TT] = hsub(dst[t + q * TT], hmul(uR[q][KC - 1], vr));
+      }
+      if (cr == 0 && t == 0) {
+        J.row_piv[static_cast<long long>(b) * kmax + r] = p;
+        J.col_piv[static_cast<long long>(b) * kmax + r] = cstar;
+      }
+      k_eff = r + 1;
+      __syncthreads();
+    }
+    // factors: own rows of U; V past k_eff zeroed (columns split over the cluster)
+#pragma unroll
+    for (int j = 0; j < KC; ++j) {
+      const int l = j - (KC - k_eff);
+      if (l >= 0) {
+#pragma unroll
+        for (int q = 0; q < RPL; ++q)
+          if (rv[q]) U[uix(l, row0 + t + q * TT)] = uR[q][j];
+      }
+    }
+    for (int l = k_eff; l < kmax; ++l)
+#pragma unroll
+      for (int q = 0; q < RPL; ++q)
+        if (rv[q]) U[uix(l, row0 + t + q * TT)] = 0.0;
+    if (k_eff < kmax)
+      for (int j = cr * TT + t; j < n; j += CL * TT)
+        for (int l = k_eff; l < kmax; ++l) V[static_cast<long long>(j) * kmax + l] = 0.0;
+    if (cr == 0) {
+      for (int l = k_eff + t; l < kmax; l += TT) {
+        J.row_piv[static_cast<long long>(b) * kmax + l] = -1;
+        J.col_piv[static_cast<long long>(b) * kmax + l] = -1;
+      }
+      if (t == 0) {
+        J.k_eff[b] = k_eff;
+        if (J.rejections && rejections) atomicAdd(J.rejections, rejections);
+        if (J.evals) {
+          atomicAdd(J.evals, ev_col);
+          atomicAdd(J.evals + 1, ev_row);
+          atomicAdd(J.evals + 2, 1ull);
+        }
+      }
+    }
+    cluster.sync();
+  }
+}
+
+template <int DIM, int KIND, int KC, int CL>
+void launch_cluster(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, cudaStream_t s) {
+  if (J.njobs <= 0) return;
+  constexpr int W = 16, NCAP = 512;
+  const size_t smem = sizeof(double) * (W * (NCAP + 1) + KC + W + W / 2 + 16 + 12 + 2 + W / 2 + NCAP / 8 + 8 + W + NCAP);
+  auto kfn = aca_cluster_kernel<DIM, KIND, KC, CL>;
+  HM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  // one cluster per SM-group: CTAs = CL * min(jobs, SMs / CL * 2)
+  const long long clusters = std::min<long long>(J.njobs, std::max(1, 2 * sms / CL));
+  kfn<<<static_cast<unsigned>(clusters * CL), 256, smem, s>>>(J, E);
+  HM_LAUNCH_CHECK();
+}
+
 template <int DIM, int KIND, int KC>
 void launch_big(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int max_rows, int sms, cudaStream_t s) {
   if (J.njobs <= 0) return;
@@ -1356,22 +1750,27 @@ void launch_team(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, cuda
 
 // ACA size classes: team kernels for max(m, n) <= 64 * NW (NW = 1, 2, 4, 8), the
 // CTA kernel for larger blocks, for k > 32 and for the epsilon criterion.
-constexpr int kAcaClasses = 7;
-constexpr int kAcaBig = 5;                // aca_big_kernel
+constexpr int kAcaClasses = 9;
+constexpr int kAcaCl4 = 5;                // aca_cluster_kernel, 4 CTAs (<= 2048 rows)
+constexpr int kAcaCl8 = 6;                // aca_cluster_kernel, 8 CTAs (<= 4096 rows)
+constexpr int kAcaBig = 7;                // aca_big_kernel
 constexpr int kAcaCta = kAcaClasses - 1;  // the general CTA kernel (epsilon criterion, k > 32)
-__host__ __device__ inline int aca_class(int m, int n, long long kmax, bool has_eps) {
+__host__ __device__ inline int aca_class(int m, int n, long long kmax, bool has_eps, bool clusters = true) {
   if (has_eps || kmax > 32) return kAcaCta;
   const int c = m > n ? m : n;
-  return c <= 64 ? 0 : c <= 128 ? 1 : c <= 256 ? 2 : c <= 512 ? 3 : c <= 1024 ? 4 : kAcaBig;
+  if (c <= 1024) return c <= 64 ? 0 : c <= 128 ? 1 : c <= 256 ? 2 : c <= 512 ? 3 : 4;
+  if (clusters && c <= 2048) return kAcaCl4;
+  if (clusters && c <= 4096) return kAcaCl8;
+  return kAcaBig;
 }
 
 __global__ void class_key_kernel(const int* __restrict__ m, const int* __restrict__ nn, long long begin, long long cnt,
-                                 int kmax, int has_eps, unsigned long long* __restrict__ keys,
+                                 int kmax, int has_eps, int clusters, unsigned long long* __restrict__ keys,
                                  unsigned* __restrict__ vals) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < cnt;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long b = begin + i;
-    const int cls = aca_class(m[b], nn[b], kmax, has_eps != 0);
+    const int cls = aca_class(m[b], nn[b], kmax, has_eps != 0, clusters != 0);
     keys[i] = (static_cast<unsigned long long>(cls) << 32) | static_cast<unsigned long long>(0x7fffffff - nn[b]);
     vals[i] = static_cast<unsigned>(b);
   }
@@ -1446,12 +1845,15 @@ void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStrea
   J.tile_shift = h.u_tile_shift;
   // size classes (team kernels for small blocks, the CTA kernel for the rest)
   const bool eps = h.cfg.has_epsilon;
+  const bool clus = std::getenv("HM_NO_CLUSTER") == nullptr;
   long long ccount[kAcaClasses] = {};
-  for (long long b = leaf_begin; b < leaf_end; ++b) ++ccount[aca_class(h.aca.h_m[b], h.aca.h_n[b], h.cfg.k, eps)];
+  for (long long b = leaf_begin; b < leaf_end; ++b)
+    ++ccount[aca_class(h.aca.h_m[b], h.aca.h_n[b], h.cfg.k, eps, clus)];
   DevBuf<int> jobs;
   jobs.alloc(cnt, s);
   class_key_kernel<<<grid_for(cnt, 256, 1 << 16), 256, 0, s>>>(h.aca.m.get(), h.aca.n.get(), leaf_begin, cnt,
-                                                                static_cast<int>(h.cfg.k), eps ? 1 : 0, keys.get(),
+                                                                static_cast<int>(h.cfg.k), eps ? 1 : 0, clus ? 1 : 0,
+                                                                keys.get(),
                                                                 reinterpret_cast<unsigned*>(jobs.get()));
   HM_LAUNCH_CHECK();
   radix_sort_pairs(keys.get(), reinterpret_cast<unsigned*>(jobs.get()), cnt, s);
@@ -1504,10 +1906,19 @@ void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStrea
     constexpr int KIND = decltype(kindc)::value;
     KernelEntry<DIM, KIND> E{h.coords.get(), h.n, h.d, h.kp};
     const bool team = std::getenv("HM_ACA_TEAM") != nullptr;  // A/B: register-window kernels
+    if (h.cfg.k <= 16) {
+      launch_cluster<DIM, KIND, 16, 4>(sub(kAcaCl4), E, sms, s);
+      launch_cluster<DIM, KIND, 16, 8>(sub(kAcaCl8), E, sms, s);
+    } else {
+      launch_cluster<DIM, KIND, 32, 4>(sub(kAcaCl4), E, sms, s);
+      launch_cluster<DIM, KIND, 32, 8>(sub(kAcaCl8), E, sms, s);
+    }
+    tr.mark("clusters (<=4096)", s);
     if (ccount[kAcaBig] > 0) {
       int max_rows = 0;
       for (long long b = leaf_begin; b < leaf_end; ++b)
-        if (aca_class(h.aca.h_m[b], h.aca.h_n[b], h.cfg.k, eps) == kAcaBig) max_rows = std::max(max_rows, h.aca.h_m[b]);
+        if (aca_class(h.aca.h_m[b], h.aca.h_n[b], h.cfg.k, eps, clus) == kAcaBig)
+          max_rows = std::max(max_rows, h.aca.h_m[b]);
       if (tr.on && std::getenv("HM_TRACE_BIG")) {  // per-size sub-launches (jobs are sorted by n descending)
         const int edges[] = {1 << 30, 16384, 8192, 4096, 2048, 0};
         AcaJob Jb = sub(kAcaBig);
@@ -1515,7 +1926,7 @@ void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStrea
         for (int e = 0; e < 5; ++e) {
           long long c = 0;
           for (long long b = leaf_begin; b < leaf_end; ++b)
-            if (aca_class(h.aca.h_m[b], h.aca.h_n[b], h.cfg.k, eps) == kAcaBig && h.aca.h_n[b] < edges[e] &&
+            if (aca_class(h.aca.h_m[b], h.aca.h_n[b], h.cfg.k, eps, clus) == kAcaBig && h.aca.h_n[b] < edges[e] &&
                 h.aca.h_n[b] >= edges[e + 1])
               ++c;
           AcaJob Je = Jb;
@@ -1579,8 +1990,8 @@ void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStrea
   }
   tr.mark("join", s);
   if (tr.on)
-    std::fprintf(stderr, "[hm_trace] aca classes: %lld %lld %lld %lld %lld %lld %lld\n", ccount[0], ccount[1],
-                 ccount[2], ccount[3], ccount[4], ccount[5], ccount[6]);
+    std::fprintf(stderr, "[hm_trace] aca classes: %lld %lld %lld %lld %lld | cl4 %lld cl8 %lld big %lld cta %lld\n",
+                 ccount[0], ccount[1], ccount[2], ccount[3], ccount[4], ccount[5], ccount[6], ccount[7], ccount[8]);
   tr.dump();
   tra.dump();
   if (tr.on) {

@@ -187,10 +187,12 @@ def test_halton_and_force_dense(gpu, oracle):
     (5000, 3, 40, 0, 24),      # k > 16: the 32-wide register rank window
     (6000, 2, 100, 1, 12),     # Matern, non-power-of-two clusters up to 750 wide
     (60000, 1, 64, 0, 16),     # d = 1: blocks of 15000 rows (global window column of the big kernel)
+    (40000, 2, 100, 0, 24),    # ragged 1250..5000-row blocks: 4- and 8-CTA cluster kernels, k > 16
 ])
 def test_aca_size_classes_bitwise(built, n, d, c_leaf, kind, k):
-    """Every ACA size class (window kernels for max(m,n) <= 64/128/256/512/1024, the
-    big-block kernel beyond) reproduces aca_batched's pivots, ranks and factors bit for bit."""
+    """Every ACA size class (window kernels for max(m,n) <= 64/128/256/512/1024, thread-block
+    cluster kernels <= 2048/4096, the big-block kernel beyond) reproduces aca_batched's
+    pivots, ranks and factors bit for bit."""
     P, h, o = built(n, d, c_leaf, kind, k=k)
     r0 = h.stats()["aca_rejections"]
     fh = h.aca_factors()
