@@ -128,6 +128,7 @@ void setup_common(hm_handle* H, const double* coords_dev, long long n, int d) {
   h.tm.aca_ms = ms_since(ta);
   const auto tn = Clock::now();
   if (h.cfg.near_stored) store_near_field(h, h.stream);
+  else plan_near_pairs(h, h.stream);
   HM_CUDA(cudaStreamSynchronize(h.stream));
   h.tm.near_ms = ms_since(tn);
   h.tm.setup_ms = ms_since(t0);

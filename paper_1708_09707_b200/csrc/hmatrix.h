@@ -120,6 +120,7 @@ struct HMatrix {
   // dense products of BOTH leaves of the pair into part (S doubles per dense leaf);
   // the row product then folds those partials in leaf order (hmatrix.cpp:80-104).
   bool near_sym = false;
+  bool near_sym_rc = false;  // same pairing for the recomputed (matrix-free) near field
   long long n_pairs = 0;
   DevBuf<int> pair_leaf, pair_mirror;  // stored leaf, mirror leaf (-1: diagonal or not own)
   DevBuf<int4> pair_desc;              // {leaf, first stored column, col.lower, row.lower}
@@ -158,6 +159,7 @@ void mvp_multi_morton(HMatrix& h, int R, int flags, cudaStream_t s);
 void morton_codes_device(const double* coords, long long n, int d, unsigned long long* codes, cudaStream_t s);
 void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStream_t s);
 void store_near_field(HMatrix& h, cudaStream_t s);
+void plan_near_pairs(HMatrix& h, cudaStream_t s);
 void plan_far_field(HMatrix& h, cudaStream_t s);
 // explicit-matrix ACA seam (aca.cpp:567-578) on the GPU
 void aca_dense_blocks(long long nblocks, const long long* shapes, const double* entries_host, long long kmax,

@@ -129,6 +129,8 @@ struct RowArgs {
   const long long* d_off;        // stored mode
   long long d_off_base;
   const double* d_vals;
+  const double* part;            // NEAR == 3: per-dense-leaf products (S per leaf)
+  int S;
   // aca list (window [a_lo, a_hi) of leaves)
   const int* a_rl;
   const int* a_m;
@@ -173,6 +175,10 @@ __global__ void __launch_bounds__(256) rows_kernel(RowArgs a) {
         const int rs = __ldg(a.dspans + 2 * p), re = __ldg(a.dspans + 2 * p + 1);
         for (int L = rs; L < re; ++L) {
           const int r0 = a.d_rl[L], mb = a.d_m[L], c0 = a.d_cl[L], nb = a.d_n[L];
+          if constexpr (NEAR == 3) {  // symmetric near field: the leaf's product, leaf order
+            z = hadd(z, a.part[static_cast<long long>(L) * a.S + (i - r0)]);
+            continue;
+          }
           const double* x = a.xm + c0;
           double y = 0.0;
           if constexpr (NEAR == 2) {
@@ -419,6 +425,61 @@ __global__ void __launch_bounds__(S) near_pair_kernel(const __grid_constant__ CU
   }
 }
 
+// Symmetric RECOMPUTED near field (matrix-free, regular geometry): one CTA of S threads
+// per pair of mirrored S x S dense leaves.  Thread t evaluates row t of B = A(tau, sigma)
+// once (entries bitwise equal to A(sigma, tau)^T, dx^2 being sign-symmetric), folds it
+// against x_sigma as it goes (leaf (tau, sigma)), and stores it to a padded tile from which
+// thread t then folds column t against x_tau (leaf (sigma, tau)): half the kernel
+// evaluations of the reference's two dense GEMVs, the same sequential sums.
+template <int DIM, int S>
+__global__ void __launch_bounds__(S) near_pair_rc_kernel(const int* __restrict__ list,
+                                                         const int* __restrict__ mirror, long long cnt,
+                                                         const int* __restrict__ rl, const int* __restrict__ cl,
+                                                         const double* __restrict__ coords, long long n, int d,
+                                                         KernelParams kp, const double* __restrict__ xm,
+                                                         double* __restrict__ part) {
+  constexpr int PS = S + 1;
+  constexpr int YD = DIM > 0 ? DIM : 20;
+  __shared__ double sB[S * PS];
+  __shared__ double scol[YD * S];  // column points (SoA)
+  __shared__ double sxs[S], sxt[S];
+  const int tid = threadIdx.x;
+  const int dd = DIM > 0 ? DIM : d;
+  for (long long q = blockIdx.x; q < cnt; q += gridDim.x) {
+    const int L = list[q], M = mirror[q];
+    const int r0 = rl[L], c0 = cl[L];
+    double yi[YD];
+    for (int a = 0; a < dd; ++a) {
+      yi[a] = coords[a * n + r0 + tid];
+      scol[a * S + tid] = coords[a * n + c0 + tid];
+    }
+    sxs[tid] = xm[c0 + tid];
+    sxt[tid] = xm[r0 + tid];
+    __syncthreads();
+    double y = 0.0;
+    for (int j = 0; j < S; ++j) {
+      double r2 = 0.0;
+#pragma unroll
+      for (int a = 0; a < YD; ++a) {
+        if (a >= dd) break;
+        const double dx = hsub(yi[a], scol[a * S + j]);
+        r2 = hadd(r2, hmul(dx, dx));
+      }
+      const double av = phi_r2(kp, r2);
+      y = hadd(y, hmul(av, sxs[j]));
+      sB[j * PS + tid] = av;
+    }
+    part[static_cast<long long>(L) * S + tid] = y;
+    __syncthreads();
+    if (M >= 0) {
+      double y2 = 0.0;
+      for (int i = 0; i < S; ++i) y2 = hadd(y2, hmul(sB[tid * PS + i], sxt[i]));  // B(i, tid)
+      part[static_cast<long long>(M) * S + tid] = y2;
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void pair_desc_kernel(const int* __restrict__ list, long long cnt, const int* __restrict__ rl,
                                  const int* __restrict__ cl, const long long* __restrict__ off, int S,
                                  int4* __restrict__ desc) {
@@ -609,7 +670,9 @@ void launch_rows(const RowArgs& a, int near, bool far, cudaStream_t s) {
   if (rows <= 0) return;
   const unsigned grid = grid_for(rows, 256);
 #define HM_ROWS(NEAR, FAR) rows_kernel<DIM, NEAR, FAR><<<grid, 256, 0, s>>>(a)
-  if (near == 2 && far) HM_ROWS(2, true);
+  if (near == 3 && far) HM_ROWS(3, true);
+  else if (near == 3) HM_ROWS(3, false);
+  else if (near == 2 && far) HM_ROWS(2, true);
   else if (near == 2) HM_ROWS(2, false);
   else if (near == 1 && far) HM_ROWS(1, true);
   else if (near == 1) HM_ROWS(1, false);
@@ -652,6 +715,8 @@ RowArgs base_row_args(HMatrix& h) {
   a.d_re = h.dense.run_end.get();
   a.d_off = h.dense_off.get();
   a.d_vals = h.dense_vals.get();
+  a.part = h.part.get();
+  a.S = static_cast<int>(h.n >> h.dmax_leaf);
   a.a_rl = h.aca.rl.get();
   a.a_m = h.aca.m.get();
   a.a_rs = h.aca.run_start.get();
@@ -1143,6 +1208,56 @@ static CUtensorMap near_tensor_map(const HMatrix& h, int S) {
   return m;
 }
 
+// Recompute (matrix-free) near field in regular geometry: the pair list of the symmetric
+// layout without storing any block (near_pair_rc_kernel evaluates each pair once).
+void plan_near_pairs(HMatrix& h, cudaStream_t s) {
+  h.near_sym_rc = false;
+  if (h.cfg.near_stored || std::getenv("HM_NO_SYM") != nullptr) return;
+  const long long S = h.n >> h.dmax_leaf;
+  if (S != 32 && S != 64) return;
+  long long lo, hi;
+  own_range(h.dense, h.row_begin, h.row_end, lo, hi);
+  for (long long b = lo; b < hi; ++b)
+    if (h.dense.h_m[b] != S || h.dense.h_n[b] != S) return;
+  std::vector<int> list;
+  for (long long b = lo; b < hi; ++b) {
+    const long long r0 = h.dense.h_rl[b], c0 = h.dense.h_cl[b];
+    if (!(r0 > c0 && c0 >= h.row_begin && c0 < h.row_end)) list.push_back(static_cast<int>(b));
+  }
+  h.n_pairs = static_cast<long long>(list.size());
+  h.pair_leaf.alloc(std::max<size_t>(list.size(), 1), s);
+  h.pair_mirror.alloc(std::max<size_t>(list.size(), 1), s);
+  if (!list.empty())
+    HM_CUDA(cudaMemcpyAsync(h.pair_leaf.get(), list.data(), sizeof(int) * list.size(), cudaMemcpyHostToDevice, s));
+  mirror_kernel<<<grid_for(h.n_pairs, 256, 1 << 16), 256, 0, s>>>(h.pair_leaf.get(), h.n_pairs, h.dense.rl.get(),
+                                                                   h.dense.cl.get(), h.dense.count, h.row_begin,
+                                                                   h.row_end, h.pair_mirror.get());
+  HM_LAUNCH_CHECK();
+  h.part.alloc(std::max(h.dense.count * S, 1ll), s);
+  HM_CUDA(cudaStreamSynchronize(s));  // the host list is freed on return
+  h.near_sym_rc = true;
+}
+
+template <int S>
+void launch_near_pairs_rc(HMatrix& h, cudaStream_t s) {
+  int sms = 0;
+  HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h.device));
+  const unsigned grid = static_cast<unsigned>(std::min<long long>(std::max(h.n_pairs, 1ll), sms * 16ll));
+#define HM_PRC(D)                                                                                               \
+  near_pair_rc_kernel<D, S><<<grid, S, 0, s>>>(h.pair_leaf.get(), h.pair_mirror.get(), h.n_pairs,              \
+                                               h.dense.rl.get(), h.dense.cl.get(), h.coords.get(), h.n, h.d, \
+                                               h.kp, h.xm.get(), h.part.get())
+  switch (h.d) {
+    case 1: HM_PRC(1); break;
+    case 2: HM_PRC(2); break;
+    case 3: HM_PRC(3); break;
+    case 4: HM_PRC(4); break;
+    default: HM_PRC(0); break;
+  }
+#undef HM_PRC
+  HM_LAUNCH_CHECK();
+}
+
 template <int S>
 void launch_near_pairs(HMatrix& h, cudaStream_t s) {
   constexpr int NST = 2;  // 2 x 34 KB per CTA -> 3 CTAs (6 blocks in flight) per SM
@@ -1272,6 +1387,12 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
       else if (h.cfg.k <= 16) rows_tma_kernel<32, 16, 8><<<ncl, 32, 0, s>>>(A);
       else rows_tma_kernel<32, 32, 5><<<ncl, 32, 0, s>>>(A);
       HM_LAUNCH_CHECK();
+    } else if (h.near_sym_rc && near == 1) {
+      if (h.n_pairs > 0) {
+        if ((h.n >> h.dmax_leaf) == 64) launch_near_pairs_rc<64>(h, s);
+        else launch_near_pairs_rc<32>(h, s);
+      }
+      dispatch_rows(h, a, 3, true, s);
     } else {
       dispatch_rows(h, a, near, true, s);
     }
@@ -1280,7 +1401,15 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
   }
   // recompute mode (reference default): near field first, then ACA chunk by chunk
   h.clk.start(kKRows, s);
-  dispatch_rows(h, a, near, false, s);
+  if (h.near_sym_rc && near == 1) {
+    if (h.n_pairs > 0) {
+      if ((h.n >> h.dmax_leaf) == 64) launch_near_pairs_rc<64>(h, s);
+      else launch_near_pairs_rc<32>(h, s);
+    }
+    dispatch_rows(h, a, 3, false, s);
+  } else {
+    dispatch_rows(h, a, near, false, s);
+  }
   h.clk.stop(kKRows, s);
   const long long kmax = h.cfg.k;
   // chunk budget: U+V bytes
