@@ -1093,7 +1093,7 @@ constexpr int kBigThreads = 256;
 constexpr int kBigW = 8;
 
 template <int DIM, int KIND, int KC>
-__global__ void __launch_bounds__(kBigThreads) aca_big_kernel(AcaJob J, KernelEntry<DIM, KIND> E, double* gscratch,
+__global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, KernelEntry<DIM, KIND> E, double* gscratch,
                                                               long long gstride, int mask_words) {
   constexpr int TT = kBigThreads;
   constexpr int W = kBigW;

@@ -1434,11 +1434,21 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
     HM_CUDA(cudaMemcpyAsync(&ue, h.u_off.get() + c1, sizeof(long long), cudaMemcpyDeviceToHost, s));
     HM_CUDA(cudaMemcpyAsync(&ve, h.v_off.get() + c1, sizeof(long long), cudaMemcpyDeviceToHost, s));
     HM_CUDA(cudaStreamSynchronize(s));
+    const bool trace = std::getenv("HM_TRACE") != nullptr;
+    const auto tc0 = std::chrono::steady_clock::now();
     if (h.U.size() < static_cast<size_t>(ue - ub)) h.U.alloc(ue - ub, s);
     if (h.V.size() < static_cast<size_t>(ve - vb)) h.V.alloc(ve - vb, s);
+    const auto tc1 = std::chrono::steady_clock::now();
     h.clk.start(kKAca, s);
     compute_aca(h, c0, c1, s);
     h.clk.stop(kKAca, s);
+    if (trace) {
+      HM_CUDA(cudaStreamSynchronize(s));
+      const auto tc2 = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[hm_trace] chunk [%lld,%lld) %.1f GB: alloc %.1f ms, aca (host wall) %.1f ms\n", c0, c1,
+                   bytes / 1e9, std::chrono::duration<double, std::milli>(tc1 - tc0).count(),
+                   std::chrono::duration<double, std::milli>(tc2 - tc1).count());
+    }
     h.clk.start(kKLowrankT, s);
     launch_t(h, c1 - c0, vb, s);
     h.clk.stop(kKLowrankT, s);
