@@ -14,14 +14,21 @@
 // Every rejected column is consumed, so the consumed columns always form a
 // prefix: the per-block state is a single "next column" pointer.
 //
-// B200 mapping: one CTA (256 threads) per block, persistent over a largest-first
-// queue.  The CTA is split into W = 256/G column groups of G threads
-// (G = clamp(pow2ceil(m), 32, 256)) so small blocks evaluate W candidate
-// columns per wave; the lowest qualifying index wins, exactly reproducing the
-// sequential scan.  Entries are bit-identical to the host (glibc exp port, no
-// FMA contraction), so u/v and the pivots are bitwise the reference's.  The only
-// order-sensitive quantity, norm2, is summed in parallel with a rigorous error
-// bound; decisions inside the bound fall back to the reference's sequential fold.
+// B200 mapping: blocks are binned by max(m, n) and each bin runs its own persistent
+// kernel over a largest-first queue (compute_aca):
+//   <= 64 .. 1024 rows   aca_win_kernel     team of NW = 1..16 warps per block, rows in
+//                                           registers, shared-memory window of candidate
+//                                           columns (speculative, nothing re-evaluated)
+//   <= 2048 / 4096       aca_cluster_kernel thread-block cluster of 4 / 8 CTAs, partials
+//                                           and pivots exchanged through distributed
+//                                           shared memory
+//   larger               aca_big_kernel     one CTA, L2-resident window column scratch
+//   epsilon, k > 32      aca_kernel         the general CTA-per-block path
+// Entries are bit-identical to the host (glibc exp/log ports, no FMA contraction), the
+// residual chains run in the reference's order (aca_chain.cuh), so u/v and the pivots
+// are bitwise the reference's.  The only order-sensitive quantities, norm2 and scale2,
+// are summed in parallel with a rigorous error bound; decisions inside the bound fall
+// back to the reference's sequential folds.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -390,337 +397,13 @@ void launch_kernel_aca(const AcaJob& J, const HMatrix& h, cudaStream_t s) {
   HM_LAUNCH_CHECK();
 }
 
-// ---------------------------------------------------------------------------
-// Team kernel: the same per-block semantics with the block's residual columns in
-// REGISTERS.  A team of NW warps owns one block (m, n <= 64*NW); thread t of the
-// team owns rows t and t + 32*NW, and keeps u_l of its rows in registers (u[l][q]).
-// v_l is kept in shared memory rank-major (s_v[l][j]) so the column scan reads it
-// as a broadcast.  Candidate columns are evaluated W at a time (speculatively):
-// the lowest qualifying one is accepted, the ones before it are consumed, and the
-// ones after it stay cached in registers and receive the single update
-// u_r * v_r[c] of the accepted cross -- the same chain of mul-then-sub steps the
-// reference applies to a freshly evaluated column (aca.cpp:363-364), so the bits
-// are identical while no evaluated entry is wasted.  Reductions are warp
-// butterflies (every lane ends with the same value), combined across the NW warps
-// in warp order through shared memory.
+// Team barrier: a warp (NW = 1) or a named barrier over the team's NW warps.
 template <int NW>
 __device__ __forceinline__ void team_sync(int team) {
   if constexpr (NW == 1) {
     __syncwarp();
   } else {
     asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(NW * 32) : "memory");
-  }
-}
-
-// shared doubles per team: s_v (KC x 64NW), s_col (64NW), s_up (KC), 3 x NW*W partials, misc
-template <int NW, int KC, int W>
-__host__ __device__ constexpr size_t team_stride() {
-  return static_cast<size_t>(KC) * NW * 64 + NW * 64 + KC + 3 * NW * W + 4;
-}
-
-template <int DIM, int KIND, int NW, int KC, int W>
-__global__ void __launch_bounds__(256) aca_team_kernel(AcaJob J, KernelEntry<DIM, KIND> E, int teams_per_cta) {
-  constexpr int RPL = 2;
-  constexpr int TT = NW * 32;   // threads per team
-  constexpr int NCAP = TT * RPL;
-  constexpr int YD = DIM > 0 ? DIM : 1;
-  extern __shared__ double smem[];
-  const int team = threadIdx.x / TT, t = threadIdx.x % TT, lane = t & 31, wib = t >> 5;
-  if (team >= teams_per_cta) return;
-  constexpr int kRed = NW * W;  // per-warp partials
-  double* base = smem + static_cast<size_t>(team) * team_stride<NW, KC, W>();
-  double* s_v = base;                   // KC x NCAP, rank-major
-  double* s_col = s_v + KC * NCAP;      // NCAP (exact folds)
-  double* s_up = s_col + NCAP;          // KC: u_l[p] of the pivot row
-  double* s_rsum = s_up + KC;           // kRed partial sums
-  double* s_rbv = s_rsum + kRed;        // kRed partial maxima
-  int* s_rbi = reinterpret_cast<int*>(s_rbv + kRed);  // kRed ints
-  double* s_misc = s_rbv + kRed + (kRed + 1) / 2;      // [0] pivot value, [1] job, [2] scale, [3] flags
-  const double kEps0sq = 1e-14 * 1e-14;
-  const int kmax = J.kmax;
-
-  for (;;) {
-    if (t == 0) s_misc[1] = static_cast<double>(atomicAdd(J.counter, 1));
-    team_sync<NW>(team);
-    const long long job = static_cast<long long>(s_misc[1]);
-    team_sync<NW>(team);
-    if (job >= J.njobs) return;
-    const int b = J.order[job];
-    const int rl = J.rl[b], m = J.m[b], cl = J.cl[b], n = J.nn[b];
-    double* U = J.U + (J.u_off[b] - J.u_base);
-    double* V = J.V + (J.v_off[b] - J.v_base);
-    const int tsh = J.tile_shift;
-    auto uix = [&](int l, int i) -> long long {
-      if (tsh < 0) return static_cast<long long>(l) * m + i;
-      return ((static_cast<long long>(i >> tsh) * kmax + l) << tsh) + (i & ((1 << tsh) - 1));
-    };
-
-    double y[RPL][YD];
-    bool rv[RPL];
-#pragma unroll
-    for (int q = 0; q < RPL; ++q) {
-      const int i = t + q * TT;
-      rv[q] = i < m;
-      if constexpr (DIM > 0) {
-#pragma unroll
-        for (int a = 0; a < DIM; ++a) y[q][a] = rv[q] ? __ldg(E.coords + a * E.n + rl + i) : 0.0;
-      }
-    }
-    auto entry = [&](int q, long long colpt) -> double {
-      if constexpr (DIM > 0) {
-        return E.eval(y[q], colpt);
-      } else {
-        double yy[20];
-        E.load(rl + t + q * TT, yy);
-        return E.eval(yy, colpt);
-      }
-    };
-
-    // u_l of the own rows, right-aligned: at rank r, u_l lives in uR[q][KC - r + l]
-    double uR[RPL][KC];
-#pragma unroll
-    for (int q = 0; q < RPL; ++q)
-#pragma unroll
-      for (int j = 0; j < KC; ++j) uR[q][j] = 0.0;
-    double res[W][RPL];
-#pragma unroll
-    for (int w = 0; w < W; ++w)
-#pragma unroll
-      for (int q = 0; q < RPL; ++q) res[w][q] = 0.0;
-    unsigned used = 0;  // RPL bits: own rows that are pivots
-    int next = 0, cached = 0, k_eff = 0;
-    unsigned long long rejections = 0, ev_col = 0, ev_row = 0;
-    double scale = -1.0;
-    const double gm = static_cast<double>(m) * 1.2e-16;
-
-    for (int r = 0; r < kmax; ++r) {
-      int acc_w = -1;
-      double acc[RPL];
-#pragma unroll
-      for (int q = 0; q < RPL; ++q) acc[q] = 0.0;
-      const double* vb = s_v + static_cast<long long>(r - KC) * NCAP;  // chain base (see aca_chain.cuh)
-      while (next < n) {
-        const int wcols = min(W, n - next);
-        ev_col += static_cast<unsigned long long>(wcols - cached) * m;
-        // fresh evaluations of window columns [cached, wcols): entry, then the chain
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-          if (w >= cached && w < wcols) {
-            const int c = next + w;
-#pragma unroll
-            for (int q = 0; q < RPL; ++q)
-              res[w][q] = rv[q] ? Chain<KC>::run(entry(q, cl + c), uR[q], r, vb + c, NCAP) : 0.0;
-          }
-        }
-        // qualification of every window column: norm2 (parallel, bounded) and "some
-        // unused row is non-zero" (best > 0, aca.cpp:381)
-        double sum[W];
-        unsigned nzmask = 0;
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-          sum[w] = 0.0;
-          bool nz = false;
-#pragma unroll
-          for (int q = 0; q < RPL; ++q) {
-            if (rv[q]) {
-              const double a = res[w][q];
-              sum[w] = hadd(sum[w], hmul(a, a));
-              nz |= !((used >> q) & 1u) && fabs(a) > 0.0;
-            }
-          }
-#pragma unroll
-          for (int o = 16; o; o >>= 1) sum[w] = hadd(sum[w], __shfl_xor_sync(0xffffffffu, sum[w], o));
-          if (__any_sync(0xffffffffu, nz)) nzmask |= 1u << w;
-        }
-        if constexpr (NW > 1) {
-          if (lane == 0) {
-#pragma unroll
-            for (int w = 0; w < W; ++w) s_rsum[wib * W + w] = sum[w];
-            s_rbi[wib] = static_cast<int>(nzmask);
-          }
-          team_sync<NW>(team);
-          nzmask = 0;
-#pragma unroll
-          for (int w = 0; w < W; ++w) {
-            sum[w] = s_rsum[w];
-            for (int g = 1; g < NW; ++g) sum[w] = hadd(sum[w], s_rsum[g * W + w]);
-          }
-          for (int g = 0; g < NW; ++g) nzmask |= static_cast<unsigned>(s_rbi[g]);
-          team_sync<NW>(team);
-        }
-        // decision: lowest qualifying column of the window (uniform across the team)
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-          if (acc_w < 0 && w < wcols && ((nzmask >> w) & 1u)) {
-            bool qf = false;
-            if (scale < 0.0) {
-              qf = true;
-            } else {
-              const double T = hmul(kEps0sq, scale);
-              const double lo = hmul(sum[w], 1.0 - 4.0 * gm), hi = hmul(sum[w], 1.0 + 4.0 * gm);
-              if (lo > T) {
-                qf = true;
-              } else if (hi <= T) {
-                qf = false;
-              } else {  // ambiguous: the reference's sequential left fold (aca.cpp:373-374)
-#pragma unroll
-                for (int qq = 0; qq < RPL; ++qq)
-                  if (rv[qq]) s_col[t + qq * TT] = res[w][qq];
-                team_sync<NW>(team);
-                double f = hmul(s_col[0], s_col[0]);
-                for (int i = 1; i < m; ++i) f = hadd(f, hmul(s_col[i], s_col[i]));
-                team_sync<NW>(team);
-                qf = f > T;
-              }
-            }
-            if (qf) acc_w = w;
-          }
-        }
-        const int consumed = acc_w >= 0 ? acc_w + 1 : wcols;
-        rejections += static_cast<unsigned long long>(acc_w >= 0 ? acc_w : wcols);
-        if (acc_w >= 0) {
-#pragma unroll
-          for (int w = 0; w < W; ++w)
-            if (w == acc_w)
-#pragma unroll
-              for (int q = 0; q < RPL; ++q) acc[q] = res[w][q];
-        }
-        for (int sh = 0; sh < consumed; ++sh) {
-#pragma unroll
-          for (int w = 0; w + 1 < W; ++w)
-#pragma unroll
-            for (int q = 0; q < RPL; ++q) res[w][q] = res[w + 1][q];
-        }
-        cached = acc_w >= 0 ? wcols - consumed : 0;
-        next += consumed;
-        if (acc_w >= 0) break;
-      }
-      if (acc_w < 0) break;  // no usable column left (aca.cpp:442-443)
-      const int cstar = next - 1;
-
-      // pivot row: argmax |u_hat| over unused rows, first index wins (aca.cpp:367, 375-376)
-      double bv = -1.0;
-      int bi = 0x7fffffff;
-#pragma unroll
-      for (int q = 0; q < RPL; ++q) {
-        const double av = fabs(acc[q]);
-        if (rv[q] && !((used >> q) & 1u) && av > bv) {
-          bv = av;
-          bi = t + q * TT;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        argmax_combine(bv, bi, ov, oi);
-      }
-      if constexpr (NW > 1) {
-        if (lane == 0) {
-          s_rbv[wib] = bv;
-          s_rbi[wib] = bi;
-        }
-        team_sync<NW>(team);
-        bv = s_rbv[0];
-        bi = s_rbi[0];
-        for (int g = 1; g < NW; ++g) argmax_combine(bv, bi, s_rbv[g], s_rbi[g]);
-      }
-      const int p = bi;
-
-      // (first cross) scale2 = exact left fold of the column (aca.cpp:491)
-      if (r == 0) {
-#pragma unroll
-        for (int q = 0; q < RPL; ++q)
-          if (rv[q]) s_col[t + q * TT] = acc[q];
-        team_sync<NW>(team);
-        if (t == 0) {
-          double f = hmul(s_col[0], s_col[0]);
-          for (int i = 1; i < m; ++i) f = hadd(f, hmul(s_col[i], s_col[i]));
-          s_misc[2] = f;
-        }
-      }
-      const int pt = p % TT, pq = p / TT;
-      if (t == pt) {
-#pragma unroll
-        for (int q = 0; q < RPL; ++q) {
-          if (q == pq) {
-            s_misc[0] = acc[q];
-#pragma unroll
-            for (int j = 0; j < KC; ++j)
-              if (j >= KC - r) s_up[j - (KC - r)] = uR[q][j];
-          }
-        }
-        used |= 1u << pq;
-      }
-      team_sync<NW>(team);
-      if (r == 0) scale = s_misc[2];
-      const double pivot_val = s_misc[0];
-      // u_r = u_hat / pivot (aca.cpp:466-470), appended right-aligned
-#pragma unroll
-      for (int q = 0; q < RPL; ++q) {
-#pragma unroll
-        for (int j = 0; j + 1 < KC; ++j) uR[q][j] = uR[q][j + 1];
-        uR[q][KC - 1] = rv[q] ? __ddiv_rn(acc[q], pivot_val) : 0.0;
-      }
-      // v_r = A(p,:) - sum_l u_l[p] v_l (aca.cpp:474-481)
-      ev_row += n;
-      {
-        double yp[DIM > 0 ? DIM : 20];
-        E.load(rl + p, yp);
-        for (int j = t; j < n; j += TT) {
-          double a = E.eval(yp, cl + j);
-          for (int l = 0; l < r; ++l) a = hsub(a, hmul(s_up[l], s_v[l * NCAP + j]));
-          s_v[r * NCAP + j] = a;
-        }
-      }
-      team_sync<NW>(team);
-      // cached window columns receive this cross (the next step of their chain)
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        if (w < cached) {
-          const double vr = s_v[r * NCAP + next + w];
-#pragma unroll
-          for (int q = 0; q < RPL; ++q) res[w][q] = hsub(res[w][q], hmul(uR[q][KC - 1], vr));
-        }
-      }
-      if (t == 0) {
-        J.row_piv[static_cast<long long>(b) * kmax + r] = p;
-        J.col_piv[static_cast<long long>(b) * kmax + r] = cstar;
-      }
-      k_eff = r + 1;
-    }
-    // factors: U (layout uix), V interleaved n x kmax, zero past k_eff
-#pragma unroll
-    for (int j = 0; j < KC; ++j) {
-      const int l = j - (KC - k_eff);  // u_l at uR[q][KC - k_eff + l]
-      if (l >= 0) {
-#pragma unroll
-        for (int q = 0; q < RPL; ++q)
-          if (rv[q]) U[uix(l, t + q * TT)] = uR[q][j];
-      }
-    }
-    for (int l = k_eff; l < kmax; ++l)
-#pragma unroll
-      for (int q = 0; q < RPL; ++q)
-        if (rv[q]) U[uix(l, t + q * TT)] = 0.0;
-    for (int idx = t; idx < n * kmax; idx += TT) {
-      const int j = idx / kmax, l = idx - j * kmax;
-      V[idx] = l < k_eff ? s_v[l * NCAP + j] : 0.0;
-    }
-    for (int l = k_eff + t; l < kmax; l += TT) {
-      J.row_piv[static_cast<long long>(b) * kmax + l] = -1;
-      J.col_piv[static_cast<long long>(b) * kmax + l] = -1;
-    }
-    if (t == 0) {
-      J.k_eff[b] = k_eff;
-      if (J.rejections && rejections) atomicAdd(J.rejections, rejections);
-      if (J.evals) {
-        atomicAdd(J.evals, ev_col);
-        atomicAdd(J.evals + 1, ev_row);
-        atomicAdd(J.evals + 2, 1ull);
-      }
-    }
-    team_sync<NW>(team);
   }
 }
 
@@ -1732,22 +1415,6 @@ void launch_big(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int max_rows, 
   HM_LAUNCH_CHECK();
 }
 
-constexpr int kTeamW = 4;  // candidate columns per wave
-
-template <int DIM, int KIND, int NW, int KC>
-void launch_team(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, cudaStream_t s) {
-  if (J.njobs <= 0) return;
-  constexpr int teams = NW >= 4 ? 1 : 4 / NW;
-  const size_t smem = teams * team_stride<NW, KC, kTeamW>() * sizeof(double);
-  auto kfn = aca_team_kernel<DIM, KIND, NW, KC, kTeamW>;
-  HM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  int occ = 0;
-  HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, teams * NW * 32, smem));
-  const long long ctas = std::min<long long>((J.njobs + teams - 1) / teams, static_cast<long long>(std::max(occ, 1)) * sms);
-  kfn<<<static_cast<unsigned>(std::max(ctas, 1ll)), teams * NW * 32, smem, s>>>(J, E, teams);
-  HM_LAUNCH_CHECK();
-}
-
 // ACA size classes: team kernels for max(m, n) <= 64 * NW (NW = 1, 2, 4, 8), the
 // CTA kernel for larger blocks, for k > 32 and for the epsilon criterion.
 constexpr int kAcaClasses = 9;
@@ -1905,7 +1572,6 @@ void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStrea
     constexpr int DIM = decltype(dimc)::value;
     constexpr int KIND = decltype(kindc)::value;
     KernelEntry<DIM, KIND> E{h.coords.get(), h.n, h.d, h.kp};
-    const bool team = std::getenv("HM_ACA_TEAM") != nullptr;  // A/B: register-window kernels
     if (h.cfg.k <= 16) {
       launch_cluster<DIM, KIND, 16, 4>(sub(kAcaCl4), E, sms, s);
       launch_cluster<DIM, KIND, 16, 8>(sub(kAcaCl8), E, sms, s);
@@ -1946,24 +1612,15 @@ void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStrea
       }
     }
     if (h.cfg.k <= 16) {
-      const char* v16 = std::getenv("HM_W16");
-      const char* v8 = std::getenv("HM_W8");
-      if (v16 && v16[0] == '1') launch_win<DIM, KIND, 16, 16, 16, false>(sub(4), E, sms, s);
-      else launch_win<DIM, KIND, 16, 16, 8, true>(sub(4), E, sms, s);
+      launch_win<DIM, KIND, 16, 16, 8, true>(sub(4), E, sms, s);
       tr.mark("win NW=16 (<=1024)", s);
-      if (team) launch_team<DIM, KIND, 8, 16>(sub(3), E, sms, s);
-      else if (v8 && v8[0] == '1') launch_win<DIM, KIND, 8, 16, 16, true>(sub(3), E, sms, s);
-      else if (v8 && v8[0] == '2') launch_win<DIM, KIND, 8, 16, 32, false>(sub(3), E, sms, s);
-      else launch_win<DIM, KIND, 8, 16, 16, false, 2>(sub(3), E, sms, s);
+      launch_win<DIM, KIND, 8, 16, 16, false, 2>(sub(3), E, sms, s);
       tr.mark("NW=8 (<=512)", s);
-      if (team) launch_team<DIM, KIND, 4, 16>(sub(2), E, sms, s);
-      else launch_win<DIM, KIND, 4, 16, 32, true>(sub(2), E, sms, s);
+      launch_win<DIM, KIND, 4, 16, 32, true>(sub(2), E, sms, s);
       tr.mark("NW=4 (<=256)", s);
-      if (team) launch_team<DIM, KIND, 2, 16>(sub(1), E, sms, s);
-      else launch_win<DIM, KIND, 2, 16, 16, true>(sub(1), E, sms, s);
+      launch_win<DIM, KIND, 2, 16, 16, true>(sub(1), E, sms, s);
       tr.mark("NW=2 (<=128)", s);
-      if (team) launch_team<DIM, KIND, 1, 16>(sub(0), E, sms, s);
-      else launch_win<DIM, KIND, 1, 16, 16, true>(sub(0), E, sms, s);
+      launch_win<DIM, KIND, 1, 16, 16, true>(sub(0), E, sms, s);
       tr.mark("NW=1 (<=64)", s);
     } else {
       launch_win<DIM, KIND, 16, 32, 16, false>(sub(4), E, sms, s);
