@@ -868,26 +868,47 @@ hm_status hm_get_aca(hm_handle* H, int64_t* k_eff, int64_t* row_piv, int64_t* co
       uo[b + 1] = uo[b] + kmax * h.aca.h_m[b];
       vo[b + 1] = vo[b] + kmax * h.aca.h_n[b];
     }
+    std::vector<double> hu, hv;
+    if (u || v) {
+      hu.resize(uo[cnt]);
+      hv.resize(vo[cnt]);
+    }
     if (!h.factors_valid) {
-      // recompute mode: factorise everything once into scratch (introspection only)
-      h.U.alloc(std::max(uo[cnt], 1ll), s);
-      h.V.alloc(std::max(vo[cnt], 1ll), s);
-      compute_aca(h, 0, cnt, s);
+      // recompute mode: factorise into scratch chunk by chunk (introspection only), the
+      // chunks sized like the product's (mvp.cu) so that any N that runs also factorises
+      size_t free_b = 0, total_b = 0;
+      HM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      const long long budget = std::max<long long>(1ll << 20, std::min<long long>(free_b / 2, 96ll << 30));
+      long long c0 = 0;
+      while (c0 < cnt) {
+        long long c1 = c0, bytes = 0;
+        while (c1 < cnt) {
+          const long long add = 8 * kmax * (h.aca.h_m[c1] + h.aca.h_n[c1]);
+          if (c1 > c0 && bytes + add > budget) break;
+          bytes += add;
+          ++c1;
+        }
+        if (h.U.size() < static_cast<size_t>(uo[c1] - uo[c0])) h.U.alloc(uo[c1] - uo[c0], s);
+        if (h.V.size() < static_cast<size_t>(vo[c1] - vo[c0])) h.V.alloc(vo[c1] - vo[c0], s);
+        compute_aca(h, c0, c1, s);
+        if (u || v) {
+          HM_CUDA(cudaMemcpyAsync(hu.data() + uo[c0], h.U.get(), sizeof(double) * (uo[c1] - uo[c0]),
+                                  cudaMemcpyDeviceToHost, s));
+          HM_CUDA(cudaMemcpyAsync(hv.data() + vo[c0], h.V.get(), sizeof(double) * (vo[c1] - vo[c0]),
+                                  cudaMemcpyDeviceToHost, s));
+          HM_CUDA(cudaStreamSynchronize(s));
+        }
+        c0 = c1;
+      }
+    } else if ((u || v) && cnt) {
+      HM_CUDA(cudaMemcpyAsync(hu.data(), h.U.get(), sizeof(double) * uo[cnt], cudaMemcpyDeviceToHost, s));
+      HM_CUDA(cudaMemcpyAsync(hv.data(), h.V.get(), sizeof(double) * vo[cnt], cudaMemcpyDeviceToHost, s));
     }
     std::vector<int> hk(cnt), hrp(cnt * kmax), hcp(cnt * kmax);
     if (cnt) {
       HM_CUDA(cudaMemcpyAsync(hk.data(), h.k_eff.get(), sizeof(int) * cnt, cudaMemcpyDeviceToHost, s));
       HM_CUDA(cudaMemcpyAsync(hrp.data(), h.row_piv.get(), sizeof(int) * cnt * kmax, cudaMemcpyDeviceToHost, s));
       HM_CUDA(cudaMemcpyAsync(hcp.data(), h.col_piv.get(), sizeof(int) * cnt * kmax, cudaMemcpyDeviceToHost, s));
-    }
-    std::vector<double> hu, hv;
-    if (u || v) {
-      hu.resize(uo[cnt]);
-      hv.resize(vo[cnt]);
-      if (cnt) {
-        HM_CUDA(cudaMemcpyAsync(hu.data(), h.U.get(), sizeof(double) * uo[cnt], cudaMemcpyDeviceToHost, s));
-        HM_CUDA(cudaMemcpyAsync(hv.data(), h.V.get(), sizeof(double) * vo[cnt], cudaMemcpyDeviceToHost, s));
-      }
     }
     HM_CUDA(cudaStreamSynchronize(s));
     if (!h.factors_valid) {
@@ -901,7 +922,7 @@ hm_status hm_get_aca(hm_handle* H, int64_t* k_eff, int64_t* row_piv, int64_t* co
         row_piv[b * kmax + l] = hrp[b * kmax + l];
         col_piv[b * kmax + l] = hcp[b * kmax + l];
         const bool live = l < hk[b];
-        const int sh = h.factors_valid ? h.u_tile_shift : -1;
+        const int sh = h.u_tile_shift;
         if (u)
           for (long long i = 0; i < m; ++i) {
             const long long src =

@@ -102,6 +102,7 @@ struct HMatrix {
   // TMA-pipelined cluster kernel; otherwise U is rank-major (kmax x m).
   int u_tile_shift = -1;
   bool tma_rows = false;
+  bool tma_far = false;  // recompute mode: far-field chunks on the TMA row kernel (U row-tiled)
   DevBuf<int> k_eff, row_piv, col_piv;
   DevBuf<int> aca_order;    // aca leaves by column count n, largest first
   long long aca_long_jobs = 0;  // prefix of aca_order with n >= 2048 (CTA-per-block fold path)

@@ -552,10 +552,12 @@ void mvp_multi_morton(HMatrix& h, int R, int flags, cudaStream_t s) {
   long long c0 = alo;
   while (c0 < ahi) {
     long long c1 = c0, bytes = 0;
+    long long row_hi = 0;  // rows touched by the chunk's leaves (canonical order: from rl[c0])
     while (c1 < ahi) {
       const long long add = 8 * kmax * (h.aca.h_m[c1] + h.aca.h_n[c1] + R);
       if (c1 > c0 && bytes + add > budget) break;
       bytes += add;
+      row_hi = std::max<long long>(row_hi, static_cast<long long>(h.aca.h_rl[c1]) + h.aca.h_m[c1]);
       ++c1;
     }
     long long ub = 0, vb = 0, ue = 0, ve = 0;
@@ -574,6 +576,8 @@ void mvp_multi_morton(HMatrix& h, int R, int flags, cudaStream_t s) {
     b.a_ubase = ub;
     b.a_lo = c0;
     b.a_hi = c1;
+    b.row_begin = std::max<long long>(h.row_begin, h.aca.h_rl[c0]);
+    b.row_end = std::min<long long>(h.row_end, row_hi);
     b.t_base = c0;
     b.U = h.U.get();
     b.t = h.tR.get();

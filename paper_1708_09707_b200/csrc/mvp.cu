@@ -495,6 +495,7 @@ struct TmaArgs {
   int D;
   const int* a_tslot;   // aca leaf -> row-cluster slot
   const double* part;   // symmetric near field: per-dense-leaf products (S each), nullptr: stored blocks
+  int far_only = 0;     // recompute-mode chunk: admissible leaves only, z accumulated from r.z_in
 };
 
 // Item cursor over the dense spans (column chunks of CW) then the aca spans of
@@ -525,6 +526,11 @@ __global__ void __launch_bounds__(S) rows_tma_kernel(TmaArgs A) {
 
   ItemCursor k;
   bool done_issuing = false;
+  // admissible leaves outside the window [a_lo, a_hi) (recompute-mode chunk) are skipped
+  auto clip = [&]() {
+    k.L = static_cast<int>(max(static_cast<long long>(k.L), a.a_lo));
+    k.L_end = static_cast<int>(min(static_cast<long long>(k.L_end), a.a_hi));
+  };
   auto settle = [&]() -> bool {
     for (;;) {
       if (k.p < k.p_end && k.L < k.L_end) return true;
@@ -534,6 +540,7 @@ __global__ void __launch_bounds__(S) rows_tma_kernel(TmaArgs A) {
           const int* sp = k.far ? a.aspans : a.dspans;
           k.L = __ldg(sp + 2 * k.p);
           k.L_end = __ldg(sp + 2 * k.p + 1);
+          if (k.far) clip();
           continue;
         }
       }
@@ -545,6 +552,7 @@ __global__ void __launch_bounds__(S) rows_tma_kernel(TmaArgs A) {
       if (k.p < k.p_end) {
         k.L = __ldg(a.aspans + 2 * k.p);
         k.L_end = __ldg(a.aspans + 2 * k.p + 1);
+        clip();
       }
     }
   };
@@ -610,8 +618,8 @@ __global__ void __launch_bounds__(S) rows_tma_kernel(TmaArgs A) {
   if (tid == 0) {
     k.far = false;
     k.j0 = 0;
-    k.p = __ldg(a.dspan_ptr + c);
-    k.p_end = __ldg(a.dspan_ptr + c + 1);
+    k.p = A.far_only ? 0 : __ldg(a.dspan_ptr + c);
+    k.p_end = A.far_only ? 0 : __ldg(a.dspan_ptr + c + 1);
     k.L = k.L_end = 0;
     if (k.p < k.p_end) {
       k.L = __ldg(a.dspans + 2 * k.p);
@@ -620,7 +628,7 @@ __global__ void __launch_bounds__(S) rows_tma_kernel(TmaArgs A) {
 #pragma unroll
     for (int st = 0; st < NST; ++st) issue(st);
   }
-  double z = 0.0, y = 0.0;
+  double z = a.z_in ? a.z_in[c * S + tid] : 0.0, y = 0.0;
   int st = 0;
   unsigned ph = 0;
   for (;;) {
@@ -1297,10 +1305,13 @@ void plan_far_field(HMatrix& h, cudaStream_t s) {
     const int D = h.dmax_leaf;
     const long long S = h.n >> D;
     const bool pow2 = S > 0 && (S & (S - 1)) == 0;
-    h.tma_rows = h.cfg.precompute_aca && h.cfg.near_stored && (h.n % (1ll << D)) == 0 && pow2 && S >= 32 &&
-                 S <= 64 && (kmax % 2) == 0 && std::getenv("HM_NO_TMA") == nullptr;
+    const bool regular = (h.n % (1ll << D)) == 0 && pow2 && S >= 32 && S <= 64 && (kmax % 2) == 0 && kmax <= 32 &&
+                         std::getenv("HM_NO_TMA") == nullptr;
+    h.tma_rows = regular && h.cfg.precompute_aca && h.cfg.near_stored;
+    // recompute mode: the per-chunk far field also runs on the TMA row kernel (U row-tiled)
+    h.tma_far = regular && !h.cfg.precompute_aca;
     h.u_tile_shift = -1;
-    if (h.tma_rows) {
+    if (h.tma_rows || h.tma_far) {
       int sh = 0;
       while ((1ll << sh) < S) ++sh;
       h.u_tile_shift = sh;
@@ -1422,10 +1433,12 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
   long long c0 = alo;
   while (c0 < ahi) {
     long long c1 = c0, bytes = 0;
+    long long row_hi = 0;  // rows touched by the chunk's leaves (canonical order: from rl[c0])
     while (c1 < ahi) {
       const long long add = 8 * kmax * (h.aca.h_m[c1] + h.aca.h_n[c1]);
       if (c1 > c0 && bytes + add > budget) break;
       bytes += add;
+      row_hi = std::max<long long>(row_hi, static_cast<long long>(h.aca.h_rl[c1]) + h.aca.h_m[c1]);
       ++c1;
     }
     long long ub = 0, vb = 0, ue = 0, ve = 0;
@@ -1457,8 +1470,31 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
     b.a_ubase = ub;
     b.a_lo = c0;
     b.a_hi = c1;
+    // only the rows the chunk's leaves touch (the others keep their partial sums)
+    b.row_begin = std::max<long long>(h.row_begin, h.aca.h_rl[c0]);
+    b.row_end = std::min<long long>(h.row_end, row_hi);
     h.clk.start(kKRowsFar, s);
-    dispatch_rows(h, b, 0, true, s);
+    if (h.tma_far) {
+      const long long S = h.n >> h.dmax_leaf;
+      b.row_begin = b.row_begin / S * S;
+      b.row_end = (b.row_end + S - 1) / S * S;
+      TmaArgs A;
+      A.r = b;
+      A.D = h.dmax_leaf;
+      A.a_tslot = h.aca.tau_slot.get();
+      A.part = nullptr;
+      A.far_only = 1;
+      const unsigned ncl = static_cast<unsigned>((b.row_end - b.row_begin) / S);
+      if (ncl > 0) {
+        if (S == 64 && kmax <= 16) rows_tma_kernel<64, 16, 5><<<ncl, 64, 0, s>>>(A);
+        else if (S == 64) rows_tma_kernel<64, 32, 2><<<ncl, 64, 0, s>>>(A);
+        else if (kmax <= 16) rows_tma_kernel<32, 16, 8><<<ncl, 32, 0, s>>>(A);
+        else rows_tma_kernel<32, 32, 5><<<ncl, 32, 0, s>>>(A);
+        HM_LAUNCH_CHECK();
+      }
+    } else {
+      dispatch_rows(h, b, 0, true, s);
+    }
     h.clk.stop(kKRowsFar, s);
     c0 = c1;
   }
