@@ -529,70 +529,120 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
         }
         filled = wcols;
         team_sync<NW>(team);
-        // qualification: G threads per column; state 0 no, 1 yes, 2 ambiguous
-        {
-          const int w = t / G, g = t % G;
+        // fast path while the block has rejected nothing (smooth blocks accept the first
+        // candidate of every rank): the first window column with all team threads
+        int first_state = -1;
+        if (rejections == 0) {
+          const double* src = s_win + (next % W) * PS;
           double sum = 0.0;
           int nz = 0;
-          if (w < wcols) {
-            const double* src = s_win + ((next + w) % W) * PS;
-            for (int i = g; i < m; i += G) {
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) {
+            const int i = t + q * TT;
+            if (i < m) {
               const double a = src[i];
               sum = hadd(sum, hmul(a, a));
               nz |= (!s_used[i] && fabs(a) > 0.0) ? 1 : 0;
             }
           }
 #pragma unroll
-          for (int o = GL / 2; o; o >>= 1) {
+          for (int o = 16; o; o >>= 1) {
             sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
             nz |= __shfl_xor_sync(0xffffffffu, nz, o);
           }
-          if constexpr (G > 32) {  // a column spans G/32 warps: combine their partials in warp order
+          if constexpr (NW > 1) {
             if (lane == 0) {
               s_rbv[wib] = sum;
               s_rbi[wib] = nz;
             }
             team_sync<NW>(team);
-            if (g == 0 && w < wcols) {
-              sum = s_rbv[wib];
-              nz = s_rbi[wib];
-              for (int k2 = 1; k2 < G / 32; ++k2) {
-                sum = hadd(sum, s_rbv[wib + k2]);
-                nz |= s_rbi[wib + k2];
-              }
+            sum = s_rbv[0];
+            nz = s_rbi[0];
+            for (int k2 = 1; k2 < NW; ++k2) {
+              sum = hadd(sum, s_rbv[k2]);
+              nz |= s_rbi[k2];
             }
+            team_sync<NW>(team);
           }
-          if (g == 0 && w < wcols) {
-            int st = 0;
-            if (nz) {
-              if (scale < 0.0) {
-                st = 1;
-              } else {
-                const double T = hmul(kEps0sq, scale);
-                const double lo = hmul(sum, 1.0 - 4.0 * gm), hi = hmul(sum, 1.0 + 4.0 * gm);
-                st = lo > T ? 1 : (hi <= T ? 0 : 2);
-              }
+          first_state = 0;
+          if (nz) {
+            if (scale < 0.0) {
+              first_state = 1;
+            } else {
+              const double T = hmul(kEps0sq, scale);
+              const double lo = hmul(sum, 1.0 - 4.0 * gm), hi = hmul(sum, 1.0 + 4.0 * gm);
+              first_state = lo > T ? 1 : (hi <= T ? 0 : 2);
             }
-            s_state[w] = st;
           }
         }
-        team_sync<NW>(team);
-        for (int w = 0; w < wcols; ++w) {
-          int st = s_state[w];
-          if (st == 2) {  // the reference's sequential left fold (aca.cpp:373-374 / 414-415)
-            if (t == 0) {
+        if (first_state == 1) {
+          acc_w = 0;
+        } else {
+          // qualification: G threads per column; state 0 no, 1 yes, 2 ambiguous
+          {
+            const int w = t / G, g = t % G;
+            double sum = 0.0;
+            int nz = 0;
+            if (w < wcols) {
               const double* src = s_win + ((next + w) % W) * PS;
-              double f = hmul(src[0], src[0]);
-              for (int i = 1; i < m; ++i) f = hadd(f, hmul(src[i], src[i]));
-              s_misc[2] = f > hmul(kEps0sq, scale) ? 1.0 : 0.0;
+              for (int i = g; i < m; i += G) {
+                const double a = src[i];
+                sum = hadd(sum, hmul(a, a));
+                nz |= (!s_used[i] && fabs(a) > 0.0) ? 1 : 0;
+              }
             }
-            team_sync<NW>(team);
-            st = s_misc[2] != 0.0 ? 1 : 0;
-            team_sync<NW>(team);
+  #pragma unroll
+            for (int o = GL / 2; o; o >>= 1) {
+              sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+              nz |= __shfl_xor_sync(0xffffffffu, nz, o);
+            }
+            if constexpr (G > 32) {  // a column spans G/32 warps: combine their partials in warp order
+              if (lane == 0) {
+                s_rbv[wib] = sum;
+                s_rbi[wib] = nz;
+              }
+              team_sync<NW>(team);
+              if (g == 0 && w < wcols) {
+                sum = s_rbv[wib];
+                nz = s_rbi[wib];
+                for (int k2 = 1; k2 < G / 32; ++k2) {
+                  sum = hadd(sum, s_rbv[wib + k2]);
+                  nz |= s_rbi[wib + k2];
+                }
+              }
+            }
+            if (g == 0 && w < wcols) {
+              int st = 0;
+              if (nz) {
+                if (scale < 0.0) {
+                  st = 1;
+                } else {
+                  const double T = hmul(kEps0sq, scale);
+                  const double lo = hmul(sum, 1.0 - 4.0 * gm), hi = hmul(sum, 1.0 + 4.0 * gm);
+                  st = lo > T ? 1 : (hi <= T ? 0 : 2);
+                }
+              }
+              s_state[w] = st;
+            }
           }
-          if (st == 1) {
-            acc_w = w;
-            break;
+          team_sync<NW>(team);
+          for (int w = 0; w < wcols; ++w) {
+            int st = s_state[w];
+            if (st == 2) {  // the reference's sequential left fold (aca.cpp:373-374 / 414-415)
+              if (t == 0) {
+                const double* src = s_win + ((next + w) % W) * PS;
+                double f = hmul(src[0], src[0]);
+                for (int i = 1; i < m; ++i) f = hadd(f, hmul(src[i], src[i]));
+                s_misc[2] = f > hmul(kEps0sq, scale) ? 1.0 : 0.0;
+              }
+              team_sync<NW>(team);
+              st = s_misc[2] != 0.0 ? 1 : 0;
+              team_sync<NW>(team);
+            }
+            if (st == 1) {
+              acc_w = w;
+              break;
+            }
           }
         }
         const int consumed = acc_w >= 0 ? acc_w + 1 : wcols;
@@ -1618,9 +1668,10 @@ void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStrea
       tr.mark("NW=8 (<=512)", s);
       launch_win<DIM, KIND, 4, 16, 32, true>(sub(2), E, sms, s);
       tr.mark("NW=4 (<=256)", s);
-      launch_win<DIM, KIND, 2, 16, 16, true>(sub(1), E, sms, s);
+      // the small blocks are latency-bound: registers capped for 12 / 16 warps per SM
+      launch_win<DIM, KIND, 2, 16, 16, true, 3>(sub(1), E, sms, s);
       tr.mark("NW=2 (<=128)", s);
-      launch_win<DIM, KIND, 1, 16, 16, true>(sub(0), E, sms, s);
+      launch_win<DIM, KIND, 1, 16, 8, true, 4>(sub(0), E, sms, s);
       tr.mark("NW=1 (<=64)", s);
     } else {
       launch_win<DIM, KIND, 16, 32, 16, false>(sub(4), E, sms, s);
