@@ -448,6 +448,8 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
   double* s_misc = s_rbv + 2 * NW + W + NCAP / 8;  // [0] job, [1] scale, [2] exact-fold verdict
   const double kEps0sq = 1e-14 * 1e-14;
   const int kmax = J.kmax;
+  const bool kpow2 = (kmax & (kmax - 1)) == 0;
+  const int kshift = __popc(kmax - 1);
 
   for (;;) {
     if (t == 0) s_misc[0] = static_cast<double>(atomicAdd(J.counter, 1));
@@ -774,7 +776,8 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
     if constexpr (VSM) {
       team_sync<NW>(team);
       for (int idx = t; idx < n * kmax; idx += TT) {
-        const int j = idx / kmax, l = idx - j * kmax;
+        // kmax is a power of two in practice (k = 16): shift instead of an integer division
+        const int j = kpow2 ? idx >> kshift : idx / kmax, l = idx - j * kmax;
         V[idx] = l < k_eff ? s_v[l * NCAP + j] : 0.0;
       }
     } else {
