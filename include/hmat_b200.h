@@ -35,7 +35,8 @@ typedef enum {
   HM_ECUDA = 4,      /* CUDA runtime error (also: no CUDA device)          */
   HM_ENCCL = 5,      /* NCCL error                                         */
   HM_ENONFINITE = 6, /* non-finite value (cg_solve, solver.cpp:51-54)      */
-  HM_ELOGIC = 7      /* std::logic_error / internal invariant              */
+  HM_ELOGIC = 7,     /* std::logic_error / internal invariant              */
+  HM_EIO = 8         /* std::runtime_error from file output (dump_leaves_csv) */
 } hm_status;
 
 typedef enum { HM_KERNEL_GAUSSIAN = 0, HM_KERNEL_MATERN = 1 } hm_kernel_kind;
@@ -128,7 +129,7 @@ hm_status hm_cg_solve_multi(hm_handle* h, const double* B, int64_t nrhs, double 
                             int32_t flags, double* X, int64_t* iterations, double* relative_residual);
 
 /* hmat::dump_leaves_csv (tree.hpp:94, tree.cpp:197-205): every leaf of the block tree in
- * canonical order, "row_lower,row_upper,col_lower,col_upper,admissible" (HM_ELOGIC when
+ * canonical order, "row_lower,row_upper,col_lower,col_upper,admissible" (HM_EIO when
  * the file cannot be written, the reference's runtime_error). */
 hm_status hm_dump_leaves_csv(hm_handle* h, const char* path);
 /* hmat::relative_error (hmatrix.hpp:63) -- exact product on the device, no N limit. */

@@ -36,14 +36,14 @@ _i64 = C.c_int64
 _i32 = C.c_int32
 _d = C.c_double
 
-HM_OK, HM_EINVAL, HM_ERANGE, HM_ENOMEM, HM_ECUDA, HM_ENCCL, HM_ENONFINITE, HM_ELOGIC = range(8)
+HM_OK, HM_EINVAL, HM_ERANGE, HM_ENOMEM, HM_ECUDA, HM_ENCCL, HM_ENONFINITE, HM_ELOGIC, HM_EIO = range(9)
 _STATUS_NAMES = ["HM_OK", "HM_EINVAL", "HM_ERANGE", "HM_ENOMEM", "HM_ECUDA", "HM_ENCCL", "HM_ENONFINITE",
-                 "HM_ELOGIC"]
+                 "HM_ELOGIC", "HM_EIO"]
 
 
 class HmError(RuntimeError):
     def __init__(self, status: int, msg: str):
-        super().__init__(f"{_STATUS_NAMES[status] if 0 <= status < 8 else status}: {msg}")
+        super().__init__(f"{_STATUS_NAMES[status] if 0 <= status < len(_STATUS_NAMES) else status}: {msg}")
         self.status = status
 
 

@@ -20,6 +20,7 @@ enum Status : int {
   kEnccl = 5,       // NCCL error
   kEnonfinite = 6,  // non-finite value (cg_solve, solver.cpp:51-54)
   kElogic = 7,      // std::logic_error / internal invariant
+  kEio = 8,         // std::runtime_error from file output
 };
 
 struct Error : std::runtime_error {

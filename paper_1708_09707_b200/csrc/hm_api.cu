@@ -713,7 +713,7 @@ hm_status hm_dump_leaves_csv(hm_handle* H, const char* path) {
     std::lock_guard<std::mutex> lock(H->mu);
     const HMatrix& h = H->h;
     FILE* f = std::fopen(path, "w");
-    if (!f) raise(kElogic, std::string("dump_leaves_csv: cannot open ") + path);
+    if (!f) raise(kEio, std::string("dump_leaves_csv: cannot open ") + path);
     std::fputs("row_lower,row_upper,col_lower,col_upper,admissible\n", f);
     const LeafList& D = h.dense;
     const LeafList& A = h.aca;
@@ -728,7 +728,7 @@ hm_status hm_dump_leaves_csv(hm_handle* H, const char* path) {
       std::fprintf(f, "%d,%d,%d,%d,%d\n", l.h_rl[q], l.h_rl[q] + l.h_m[q], l.h_cl[q], l.h_cl[q] + l.h_n[q],
                    take_d ? 0 : 1);
     }
-    if (std::fclose(f) != 0) raise(kElogic, std::string("dump_leaves_csv: write failed ") + path);
+    if (std::fclose(f) != 0) raise(kEio, std::string("dump_leaves_csv: write failed ") + path);
   });
 }
 
