@@ -1667,14 +1667,16 @@ void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStrea
     if (h.cfg.k <= 16) {
       launch_win<DIM, KIND, 16, 16, 8, true>(sub(4), E, sms, s);
       tr.mark("win NW=16 (<=1024)", s);
-      launch_win<DIM, KIND, 8, 16, 16, false, 2>(sub(3), E, sms, s);
+      launch_win<DIM, KIND, 8, 16, 8, true, 2>(sub(3), E, sms, s);
       tr.mark("NW=8 (<=512)", s);
-      launch_win<DIM, KIND, 4, 16, 32, true>(sub(2), E, sms, s);
+      launch_win<DIM, KIND, 4, 16, 16, true, 3>(sub(2), E, sms, s);
       tr.mark("NW=4 (<=256)", s);
-      // the small blocks are latency-bound: registers capped for 12 / 16 warps per SM
+      // the small blocks are latency-bound: registers capped for 12 warps per SM (ncu: at
+      // 208 registers / 8 warps the <= 64 class issues at IPC ~1.5, at 128 it spends 20% of
+      // its instructions rematerialising addresses; 3 CTAs per SM is the measured optimum)
       launch_win<DIM, KIND, 2, 16, 16, true, 3>(sub(1), E, sms, s);
       tr.mark("NW=2 (<=128)", s);
-      launch_win<DIM, KIND, 1, 16, 8, true, 4>(sub(0), E, sms, s);
+      launch_win<DIM, KIND, 1, 16, 8, true, 3>(sub(0), E, sms, s);
       tr.mark("NW=1 (<=64)", s);
     } else {
       launch_win<DIM, KIND, 16, 32, 16, false>(sub(4), E, sms, s);
