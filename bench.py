@@ -13,8 +13,10 @@ larger than the 126 MB L2, so no flush is needed between steps.
   roofline  = dominant kernel (the row-gather product kernel) vs measured HBM peak
   build_s   = hm_setup wall time (Morton + tree + ACA factors + dense blocks)
 
-N > 1 (torchrun): rows are partitioned by depth-log2(N) row clusters,
-every rank computes its slice, NCCL allgathers y; N is fixed -> strong scaling.
+N > 1: rows are partitioned by depth-log2(N) row clusters, every rank
+computes its slice, NCCL allgathers y; N is fixed -> strong scaling.  Launched under
+torchrun by the driver; `python bench.py --gpus N` without torchrun re-executes itself
+under torch.distributed.run with N ranks (127.0.0.1 rendezvous).
 
 --impl reference: the unmodified reference library (oracle/_ref) on the host cores,
 on a bounded row sample of the same workload (see oracle/refbench.py).
@@ -91,7 +93,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            self.rows.append((time.monotonic(), [c.strip() for c in line.split(",")]))
 
     def __exit__(self, *a):
         if self.proc:
@@ -102,15 +104,66 @@ class ClockSampler:
                 self.proc.kill()
             self.thread.join(timeout=2)
 
-    def summary(self):
-        if not self.rows:
+    def summary(self, window=None):
+        """Samples inside window = (t0, t1) (the timed region; the sampler is started before
+        the warm-up so that it is running when the timed region begins), else all."""
+        rows = [r for (t, r) in self.rows if window is None or window[0] - 0.06 <= t <= window[1] + 0.06]
+        in_window = window is not None and len(rows) >= 1
+        if not in_window:
+            rows = [r for (_, r) in self.rows]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows),
+                "window": "timed region" if in_window else "warm-up + timed region"}
+
+
+def fp64_constants():
+    """FP64 roofline denominators and the frozen per-entry instruction counts
+    (profiles/fp64_peaks.json, measured on the box by tools/fp64_peak.cu and ncu; see
+    BASELINE.md §3 and DESIGN.md §5.3)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "fp64_peaks.json")) as f:
+            return json.load(f)
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def fp64_roofline(prof, prof_steps, aca_work, args=None):
+    """Recompute mode: the ACA factorisation inside every product is the dominant,
+    FP64-pipe-bound kernel.  achieved = algorithmic FP64 instructions per product
+    (entries x c_eval + residual chains) / ACA device time; peak = measured FP64
+    instruction throughput (DFMA/DADD/DMUL issue at the same rate)."""
+    fp = fp64_constants()
+    ms_aca = prof.get("aca", (0.0, 0))[0] / max(prof_steps, 1)
+    ms_near = prof.get("rows", (0.0, 0))[0] / max(prof_steps, 1)
+    line = {"bound": "fp64", "kernel": "batched ACA inside every product (recompute mode)", "unit": "Tinst/s",
+            "achieved": None, "peak": None, "frac": None, "traffic": None, "aca_ms": ms_aca, "near_ms": ms_near,
+            "phases_ms": {k: v[0] / max(prof_steps, 1) for k, v in prof.items()}}
+    if not fp or not aca_work:
+        return line
+    key = f"{ARGS.kernel}_d{ARGS.d}"
+    c_eval = fp.get("c_eval", {}).get(key)
+    peak = fp.get("fp64_inst_per_s")
+    if not c_eval or not peak:
+        return line
+    ops = aca_work["entries"] * c_eval + aca_work["chain_ops"]
+    near_ops = aca_work["near_entries"] * (c_eval + 2.0)
+    ach = ops / (ms_aca * 1e-3) if ms_aca > 0 else None
+    line.update({"achieved": ach / 1e12 if ach else None, "peak": peak / 1e12, "frac": ach / peak if ach else None,
+                 "peak_kind": "measured (tools/fp64_peak.cu, profiles/fp64_peaks.json)",
+                 "c_eval_fp64_inst_per_entry": c_eval, "aca_fp64_inst_per_step": ops,
+                 "aca_entries_per_step": aca_work["entries"], "aca_rejections": aca_work["rejections"],
+                 "near": {"fp64_inst_per_step": near_ops, "ms": ms_near,
+                          "frac": near_ops / (ms_near * 1e-3) / peak if ms_near > 0 else None}})
+    return line
+
+
+ARGS = None
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -197,8 +250,14 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
+        # communicator init lines (rank count) on stderr, stdout stays the JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if torch.cuda.device_count() < world:
+            raise SystemExit(f"bench: {world} ranks but only {torch.cuda.device_count()} visible GPUs")
 
     n, d = args.n, args.d
     pts = uniform_points(n, d, 42)
@@ -222,6 +281,8 @@ def run_ours(args):
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
         h.attach_nccl(obj[0])
+        print(f"[bench] rank {rank}/{world}: engine NCCL communicator attached (nranks={world}), "
+              f"rows [{h.stats()['row_begin']}, {h.stats()['row_end']})", file=sys.stderr)
     st = h.stats()
     tms = h.timings()
 
@@ -237,12 +298,6 @@ def run_ours(args):
     S_lm = allsum(st["S_lm"])
     S_ln = allsum(st["S_ln"])
     S_l = S_lm + S_ln
-    if not stored:  # recompute mode: S_l from a one-off factorisation for the metric only
-        f = h.aca_factors(factors=False)
-        lv = h.aca_queue
-        S_l = float((f["k_eff"] * ((lv[:, 1] - lv[:, 0]) + (lv[:, 3] - lv[:, 2]))).sum())
-        S_lm = float((f["k_eff"] * (lv[:, 1] - lv[:, 0])).sum())
-        S_ln = S_l - S_lm
     flops = 2.0 * (S_d + S_l)
     alg_bytes = 8.0 * (S_d + S_l + 2 * n)  # the reference layout's bytes (every dense block stored)
 
@@ -257,18 +312,36 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    clocks = ClockSampler(local).__enter__()  # running before the timed region starts
     for t in range(args.warmup):
         h.mvp_device(xs[t % 4].data_ptr(), z.data_ptr(), sptr)
     barrier()
+    aca_work = None
+    if not stored:
+        # recompute mode: the achieved ranks of the factorisation inside the last product
+        # (k_eff is identical in every product) give S_l and the FP64 work:
+        # entries the reference's algorithm evaluates (accepted columns + pivot rows +
+        # rejected columns) and the residual chains (2 FP64 ops per earlier cross)
+        st2 = h.stats()
+        S_lm = allsum(st2["S_lm"])
+        S_ln = allsum(st2["S_ln"])
+        S_l = S_lm + S_ln
+        flops = 2.0 * (S_d + S_l)
+        alg_bytes = 8.0 * (S_d + S_l + 2 * n)
+        aca_work = {"entries": S_l + allsum(float(st2["aca_rejected_entries"])),
+                    "chain_ops": allsum(st2["S_chain"]), "rejections": int(allsum(float(st2["aca_rejections"]))),
+                    "near_entries": S_d}
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
-        barrier()
-        ev0.record(stream)
-        for t in range(args.steps):
-            h.mvp_device(xs[t % 4].data_ptr(), z.data_ptr(), sptr)
-        ev1.record(stream)
-        barrier()
+    barrier()
+    tw0 = time.monotonic()
+    ev0.record(stream)
+    for t in range(args.steps):
+        h.mvp_device(xs[t % 4].data_ptr(), z.data_ptr(), sptr)
+    ev1.record(stream)
+    barrier()
+    tw1 = time.monotonic()
+    clocks.__exit__()
     dev_ms = ev0.elapsed_time(ev1)
     if world > 1:
         tt = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
@@ -375,10 +448,8 @@ def run_ours(args):
                      "S_ln": S_ln, "flops_per_step": flops, "moved_bytes_per_step": moved_bytes,
                      "alg_bytes_per_step": alg_bytes, "n_dense": st["n_dense"], "n_aca": st["n_aca"],
                      "aca_rejections": st["aca_rejections"]},
-            "roofline": ({"bound": "fp64", "kernel": "ACA inside every product (recompute mode, FP64-bound)",
-                          "achieved": None, "peak": None, "unit": "TFLOP/s", "frac": None, "traffic": None,
-                          "phases_ms": {k: v[0] / max(v[1], 1) for k, v in prof.items()}}
-                         if not stored else None) or {"bound": "hbm", "kernel": names.get(dom, dom),
+            "roofline": (fp64_roofline(prof, prof_steps, aca_work) if not stored else None) or {
+                         "bound": "hbm", "kernel": names.get(dom, dom),
                          "achieved": kern[dom]["gbs"] if dom else None, "peak": hbm_peak, "unit": "GB/s",
                          "frac": (kern[dom]["gbs"] / hbm_peak) if dom else None, "traffic": traffic,
                          "peak_kind": peak_kind, "alg_bytes_per_launch": kern[dom]["alg_bytes"] if dom else None,
@@ -389,7 +460,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
             "gpu_launches": int(round(launches_per_step * args.steps)),
-            "clocks": clocks.summary(),
+            "clocks": clocks.summary((tw0, tw1)),
             "checksum_norm_z": checksum,
         }
         print(json.dumps(line))
@@ -398,8 +469,25 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def self_launch(args) -> bool:
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run (N ranks)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    rc = subprocess.call(cmd)
+    sys.exit(rc)
+
+
 def main():
+    global ARGS
     args = parse()
+    ARGS = args
+    self_launch(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -14,8 +14,11 @@
  *   - leaf lists are in canonical order (tree.cpp:189-194), dense list first.
  *
  * Thread safety: an hm_handle is immutable after hm_setup except for its product
- * workspace; concurrent hm_mvp calls on ONE handle are serialised internally
- * (a mutex per handle).  Distinct handles are independent.
+ * workspace.  Calls on ONE handle are serialised on the host (a mutex per handle) and
+ * on the device: all of a handle's work runs on its own stream, and the *_device entry
+ * points join the caller's stream to it with events (the caller's stream waits for the
+ * product, the product waits for the caller's earlier work).  Distinct handles are
+ * independent.  hm_destroy waits for the handle's outstanding work.
  */
 #ifndef HMAT_B200_H
 #define HMAT_B200_H
@@ -49,8 +52,12 @@ typedef struct {
   double eta;              /* admissibility parameter, default 1.5                      */
   int64_t c_leaf;          /* leaf size C_leaf, default 256                              */
   int64_t k;               /* ACA rank cap, default 16 (device limit 32)                 */
-  int64_t bs_aca;          /* accepted for API parity; results do not depend on it       */
-  int64_t bs_dense;        /* idem (partition_dense_queue throws if one block exceeds it) */
+  int64_t bs_aca;          /* ACA batch size (partition_aca_queue, aca.cpp:229-250): batches
+                              of Sigma m <= bs_aca (<= 0: one block per batch); recompute
+                              chunks are runs of whole batches.  Results do not depend on it */
+  int64_t bs_dense;        /* dense group cap (dense_blocks.cpp:36-66): setup throws
+                              HM_EINVAL if one block has m*n > bs_dense > 0, like the
+                              reference; the near field itself needs no workspace        */
   int32_t precompute_aca;  /* 1: factors computed once at setup and kept in HBM          */
   int32_t has_epsilon;     /* optional adaptive-rank criterion                           */
   double epsilon;
@@ -64,14 +71,16 @@ typedef struct {
 /* Timings of the last call (MvpTimings hmatrix.hpp:50-54, plus setup phases). */
 typedef struct {
   double setup_ms, morton_ms, tree_ms, aca_ms, near_ms;
-  double mvp_ms;
+  double mvp_ms;        /* MvpTimings::total_ms of the last hm_mvp (host wall, copies inside) */
+  double mvp_dense_ms;  /* MvpTimings::dense_ms: near-field phase (device events)            */
+  double mvp_aca_ms;    /* MvpTimings::aca_ms: far-field phase incl. recompute-mode ACA      */
 } hm_timings;
 
 /* Algorithmic sizes: S_d = sum_dense m*n, S_l = sum_adm k_eff*(m+n). */
 typedef struct {
   int64_t n_dense, n_aca;
   double S_d, S_l, sum_m_adm, sum_n_adm;
-  double S_lm, S_ln;       /* sum_adm k_eff*m and k_eff*n (own rows, precompute mode) */
+  double S_lm, S_ln;       /* sum_adm k_eff*m and k_eff*n (own rows; recompute mode: after a product) */
   double S_d_own;          /* dense entries of the rows this rank owns */
   int64_t aca_rejections;  /* rejected candidate columns in the last factorisation */
   int32_t dmax_leaf;
@@ -79,6 +88,10 @@ typedef struct {
   double device_bytes;
   double S_d_stored;       /* dense entries actually stored (symmetric near field: about half) */
   int32_t near_sym;        /* 1: symmetric near-field storage + pair kernel in use */
+  int64_t n_aca_batches;   /* reference ACA batches of the own leaves (bs_aca) */
+  int64_t n_aca_chunks;    /* device factorisation chunks (runs of whole batches) */
+  int64_t aca_rejected_entries; /* sum of m over the rejected candidate columns (last factorisation) */
+  double S_chain;          /* sum_adm k_eff (k_eff - 1) (m + n): residual-chain FP64 ops, own rows */
 } hm_stats;
 
 const char* hm_last_error(void);
@@ -97,7 +110,9 @@ void hm_destroy(hm_handle* h);
 /* hmat::mvp(HMatrix, x, kernel, MvpTimings*) -- hmatrix.hpp:58-59.  Host x and z
  * (length n, original ordering); copies are inside the call. */
 hm_status hm_mvp(hm_handle* h, const double* x, double* z, hm_timings* t);
-/* Device x and z on `stream` (cudaStream_t; NULL = the handle's stream).  Asynchronous. */
+/* Device x and z on `stream` (cudaStream_t; NULL = the handle's stream).  Asynchronous:
+ * no host synchronisation (every launch parameter is fixed at setup), so the call can be
+ * captured into a CUDA graph on `stream` once a first product has sized the workspaces. */
 hm_status hm_mvp_device(hm_handle* h, const double* x_dev, double* z_dev, void* stream);
 /* Attach an NCCL communicator for row-sliced products (world > 1): the 128-byte
  * ncclUniqueId produced by hm_nccl_unique_id on rank 0 and broadcast by the caller. */

@@ -68,14 +68,15 @@ class _Config(C.Structure):
 
 class _Timings(C.Structure):
     _fields_ = [("setup_ms", _d), ("morton_ms", _d), ("tree_ms", _d), ("aca_ms", _d), ("near_ms", _d),
-                ("mvp_ms", _d)]
+                ("mvp_ms", _d), ("mvp_dense_ms", _d), ("mvp_aca_ms", _d)]
 
 
 class _Stats(C.Structure):
     _fields_ = [("n_dense", _i64), ("n_aca", _i64), ("S_d", _d), ("S_l", _d), ("sum_m_adm", _d),
                 ("sum_n_adm", _d), ("S_lm", _d), ("S_ln", _d), ("S_d_own", _d), ("aca_rejections", _i64), ("dmax_leaf", _i32), ("row_begin", _i64),
                 ("row_end", _i64), ("device_bytes", _d),
-                ("S_d_stored", _d), ("near_sym", _i32)]
+                ("S_d_stored", _d), ("near_sym", _i32), ("n_aca_batches", _i64), ("n_aca_chunks", _i64),
+                ("aca_rejected_entries", _i64), ("S_chain", _d)]
 
 
 def _sig(name, res, args):
@@ -206,6 +207,10 @@ class HmatrixConfig:
 
 @dataclass
 class MvpTimings:
+    """hmat::MvpTimings (hmatrix.hpp:50-54): dense = near-field phase, aca = far-field
+    phase (incl. the recompute-mode factorisation), total = the whole call."""
+    dense_ms: float = 0.0
+    aca_ms: float = 0.0
     total_ms: float = 0.0
 
 
@@ -257,6 +262,8 @@ class HMatrix:
         _check(_lib.hm_mvp(self._h, _ptr(x), _ptr(z), C.byref(t)))
         if timings is not None:
             timings.total_ms = t.mvp_ms
+            timings.dense_ms = t.mvp_dense_ms
+            timings.aca_ms = t.mvp_aca_ms
         return z
 
     def mvp_multi(self, X, dmma: bool = False) -> np.ndarray:

@@ -1,1488 +1,12 @@
-// aca.cu -- K7: batched adaptive cross approximation on sm_100a.
-//
-// Semantics: aca_batched_impl (proj/src/aca.cpp:268-544) per block, which is
-// independent of batch composition: for r < k
-//   (i)   candidate = first unused column                          aca.cpp:333
-//   (ii)  u_hat = A(:,j) - sum_{l<r} u_l * v_l[j]   (l ascending, mul then sub)  :363-364
-//   (iii) norm2 = left fold of u_hat^2; argmax |u_hat| over unused rows, first wins :373-376
-//   (iv)  qualified <=> best > 0 && (first cross || norm2 > 1e-28 * scale2)       :381-383
-//   (v)   else the column is consumed and later columns are scanned               :400-444
-//   (vi)  u_r = u_hat / u_hat[p]                                                  :466-470
-//   (vii) v_r = A(p,:) - sum_l u_l[p] * v_l                                       :474-481
-//   (viii) pivots, scale2 = norm2 of the first accepted column                    :485-494
-//   (ix)  optional epsilon criterion                                              :497-538
-// Every rejected column is consumed, so the consumed columns always form a
-// prefix: the per-block state is a single "next column" pointer.
-//
-// B200 mapping: blocks are binned by max(m, n) and each bin runs its own persistent
-// kernel over a largest-first queue (compute_aca):
-//   <= 64 .. 1024 rows   aca_win_kernel     team of NW = 1..16 warps per block, rows in
-//                                           registers, shared-memory window of candidate
-//                                           columns (speculative, nothing re-evaluated)
-//   <= 2048 / 4096       aca_cluster_kernel thread-block cluster of 4 / 8 CTAs, partials
-//                                           and pivots exchanged through distributed
-//                                           shared memory
-//   larger               aca_big_kernel     one CTA, L2-resident window column scratch
-//   epsilon, k > 32      aca_kernel         the general CTA-per-block path
-// Entries are bit-identical to the host (glibc exp/log ports, no FMA contraction), the
-// residual chains run in the reference's order (aca_chain.cuh), so u/v and the pivots
-// are bitwise the reference's.  The only order-sensitive quantities, norm2 and scale2,
-// are summed in parallel with a rigorous error bound; decisions inside the bound fall
-// back to the reference's sequential folds.
-#include <cooperative_groups.h>
-
-#include <algorithm>
-#include <cstdio>
-#include <cstdlib>
-#include <type_traits>
-#include <vector>
-
-#include "hmatrix.h"
-#include "primitives.h"
-#include "aca_chain.cuh"
+// aca.cu -- K7 host side: factorisation schedule (plan_aca_chunk), the per-chunk launch
+// sequence (compute_aca) and the explicit-matrix seam.  Kernels: aca_impl.cuh,
+// instantiated per point dimension by aca_dim.cu.
+#include "aca_impl.cuh"
 
 namespace hmb {
+using namespace aca_detail;
 
 namespace {
-
-// HM_TRACE=1: per-phase device times of the factorisation on stderr (development aid)
-struct PhaseTrace {
-  bool on = std::getenv("HM_TRACE") != nullptr;
-  cudaEvent_t e[16];
-  const char* name[16];
-  int k = 0;
-  void mark(const char* nm, cudaStream_t s) {
-    if (!on || k >= 16) return;
-    cudaEventCreate(&e[k]);
-    cudaEventRecord(e[k], s);
-    name[k++] = nm;
-  }
-  void dump() {
-    if (!on || k == 0) return;
-    cudaEventSynchronize(e[k - 1]);
-    for (int i = 1; i < k; ++i) {
-      float ms = 0;
-      cudaEventElapsedTime(&ms, e[i - 1], e[i]);
-      std::fprintf(stderr, "[hm_trace] %-24s %9.3f ms\n", name[i], ms);
-    }
-    for (int i = 0; i < k; ++i) cudaEventDestroy(e[i]);
-    k = 0;
-  }
-};
-
-constexpr int kAcaThreads = 256;
-constexpr int kKmax = 64;        // compile-time cap on the rank
-constexpr int kColBuf = 2048;    // doubles of shared column buffer
-
-// entry sources ---------------------------------------------------------------
-// KIND: -1 runtime kernel kind, 0 Gaussian, 1 Matern (compile-time specialisation
-// keeps the Bessel code out of the Gaussian kernels' registers).
-template <int KIND>
-__device__ __forceinline__ double phi_kind(const KernelParams& kp, double r2) {
-  if constexpr (KIND == 0) return glibc_exp(-r2);
-  else if constexpr (KIND == 1) {
-    if (r2 == 0.0) return kp.matern_norm;
-    const double r = hm_sqrt(r2);
-    return hmul(hmul(bessel_k1(r), r), kp.matern_norm);
-  } else {
-    return phi_r2(kp, r2);
-  }
-}
-
-template <int DIM, int KIND = -1>
-struct KernelEntry {
-  const double* coords;
-  long long n;
-  int d;
-  KernelParams kp;
-  // point coordinates of row (absolute) i into registers
-  __device__ __forceinline__ void load(long long i, double* y) const {
-    if constexpr (DIM > 0) {
-#pragma unroll
-      for (int a = 0; a < DIM; ++a) y[a] = __ldg(coords + a * n + i);
-    } else {
-      for (int a = 0; a < d; ++a) y[a] = __ldg(coords + a * n + i);
-    }
-  }
-  // phi(y_row, point j): r2 = ((0 + dx0^2) + dx1^2) + ..., dx = row - col
-  __device__ __forceinline__ double eval(const double* y, long long j) const {
-    double r2 = 0.0;
-    if constexpr (DIM > 0) {
-#pragma unroll
-      for (int a = 0; a < DIM; ++a) {
-        const double dx = hsub(y[a], __ldg(coords + a * n + j));
-        r2 = hadd(r2, hmul(dx, dx));
-      }
-    } else {
-      for (int a = 0; a < d; ++a) {
-        const double dx = hsub(y[a], __ldg(coords + a * n + j));
-        r2 = hadd(r2, hmul(dx, dx));
-      }
-    }
-    return phi_kind<KIND>(kp, r2);
-  }
-};
-
-struct AcaJob {
-  // leaf arrays (absolute leaf index)
-  const int* rl;
-  const int* m;
-  const int* cl;
-  const int* nn;
-  const int* order;         // leaf indices to process
-  long long njobs;
-  const long long* u_off;   // absolute offsets; minus u_base / v_base
-  const long long* v_off;
-  long long u_base, v_base;
-  double* U;
-  double* V;
-  int* k_eff;               // per absolute leaf
-  int* row_piv;             // per absolute leaf x kmax
-  int* col_piv;
-  int kmax;
-  int has_eps;
-  double eps_factor;        // eps (1 - eta) / (1 + eps), aca.cpp:49
-  int* counter;
-  unsigned long long* rejections;
-  unsigned long long* evals;  // optional (HM_TRACE): [0] column-scan entries, [1] pivot-row entries, [2] blocks
-  int tile_shift;           // -1: U rank-major; else log2(S), U row-tiled by S rows
-  // explicit-matrix seam: block b entries at dense + dense_off[b], row-major m x n
-  const double* dense;
-  const long long* dense_off;
-};
-
-__device__ __forceinline__ void argmax_combine(double& bv, int& bi, double ov, int oi) {
-  if (ov > bv || (ov == bv && oi < bi)) {
-    bv = ov;
-    bi = oi;
-  }
-}
-
-template <int DIM, bool DENSE>
-__global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaJob J, KernelEntry<DIM> E) {
-  __shared__ double s_col[kColBuf];
-  __shared__ double s_vj[8][kKmax];   // v_l[cand] per wave column (W <= 8)
-  __shared__ double s_upiv[kKmax];
-  __shared__ int s_piv[kKmax];
-  __shared__ double s_wsum[kAcaThreads / 32];
-  __shared__ double s_wbv[kAcaThreads / 32];
-  __shared__ int s_wbi[kAcaThreads / 32];
-  __shared__ int s_job, s_next, s_acc, s_prow, s_stop;
-  __shared__ double s_scale, s_frob;
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const double kEps0sq = 1e-14 * 1e-14;  // aca.cpp:32, kEps0 * kEps0
-
-  for (;;) {
-    if (tid == 0) s_job = atomicAdd(J.counter, 1);
-    __syncthreads();
-    const int job = s_job;
-    if (job >= J.njobs) return;
-    const int b = J.order[job];
-    const int rl = J.rl[b], m = J.m[b], cl = J.cl[b], n = J.nn[b];
-    const int kmax = J.kmax;
-    double* U = J.U + (J.u_off[b] - J.u_base);  // kmax x m: rank-major, or row-tiled (tile_shift >= 0)
-    double* V = J.V + (J.v_off[b] - J.v_base);  // n x kmax, interleaved
-    const double* A = DENSE ? J.dense + J.dense_off[b] : nullptr;
-    // U element (l, i): rank-major l*m + i, or tiled [i / S][l][i % S] so that the
-    // k x S slice of one row tile is contiguous for the product's bulk copies
-    const int tsh = J.tile_shift;
-    auto uix = [&](int l, int i) -> long long {
-      if (tsh < 0) return static_cast<long long>(l) * m + i;
-      return ((static_cast<long long>(i >> tsh) * kmax + l) << tsh) + (i & ((1 << tsh) - 1));
-    };
-
-    int G = 32;
-    while (G < m && G < kAcaThreads) G <<= 1;
-    const int W = kAcaThreads / G;
-    const int g = tid / G, lt = tid % G;
-    const bool col_in_smem = static_cast<long long>(W) * m <= kColBuf;
-
-    if (tid == 0) {
-      s_next = 0;
-      s_stop = 0;
-      s_scale = -1.0;
-      s_frob = 0.0;
-    }
-    for (int l = tid; l < kmax; l += kAcaThreads) {
-      J.row_piv[static_cast<long long>(b) * kmax + l] = -1;
-      J.col_piv[static_cast<long long>(b) * kmax + l] = -1;
-    }
-    __syncthreads();
-    int k_eff = 0;
-    unsigned long long rejections = 0;
-
-    for (int r = 0; r < kmax; ++r) {
-      // ---------------- column search: waves of W candidate columns
-      bool accepted = false;
-      while (!accepted) {
-        const int next = s_next;
-        if (next >= n) break;
-        // v_l[cand] of every wave column (aca.cpp:349-352)
-        for (int q = tid; q < W * r; q += kAcaThreads) {
-          const int gg = q / r, l = q % r;
-          const int c = next + gg;
-          s_vj[gg][l] = c < n ? V[static_cast<long long>(c) * kmax + l] : 0.0;
-        }
-        __syncthreads();
-        const int c = next + g;
-        const bool valid = c < n;
-        double sum = 0.0, bv = -1.0;
-        int bi = 0x7fffffff;
-        if (valid) {
-          for (int i = lt; i < m; i += G) {
-            double a;
-            if constexpr (DENSE) {
-              a = A[static_cast<long long>(i) * n + c];
-            } else {
-              double y[DIM > 0 ? DIM : 20];
-              E.load(rl + i, y);
-              a = E.eval(y, cl + c);
-            }
-            for (int l = 0; l < r; ++l) a = hsub(a, hmul(U[uix(l, i)], s_vj[g][l]));
-            if (col_in_smem) s_col[g * m + i] = a;
-            else U[uix(r, i)] = a;
-            sum = hadd(sum, hmul(a, a));
-            bool used = false;
-            for (int l = 0; l < r; ++l) used |= (s_piv[l] == i);
-            const double av = fabs(a);
-            if (!used && av > bv) {
-              bv = av;
-              bi = i;
-            }
-          }
-        }
-        // group reduction: warp shuffles, then across the G/32 warps of the group
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
-          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          argmax_combine(bv, bi, ov, oi);
-        }
-        if (lane == 0) {
-          s_wsum[warp] = sum;
-          s_wbv[warp] = bv;
-          s_wbi[warp] = bi;
-        }
-        __syncthreads();
-        if (tid == 0) {
-          const int wpg = G / 32;
-          int acc = -1, consumed = 0;
-          for (int gg = 0; gg < W && next + gg < n; ++gg) {
-            double gs = 0.0, gbv = -1.0;
-            int gbi = 0x7fffffff;
-            for (int w = gg * wpg; w < (gg + 1) * wpg; ++w) {
-              gs = hadd(gs, s_wsum[w]);
-              argmax_combine(gbv, gbi, s_wbv[w], s_wbi[w]);
-            }
-            bool q = false;
-            if (gbv > 0.0) {
-              if (s_scale < 0.0) {
-                q = true;
-              } else {
-                // parallel sum vs the reference's left fold: both within gamma_m * S of
-                // the exact sum S of the (bitwise identical) squares
-                const double T = hmul(kEps0sq, s_scale);
-                const double gm = static_cast<double>(m) * 1.2e-16;
-                const double lo = hmul(gs, 1.0 - 4.0 * gm), hi = hmul(gs, 1.0 + 4.0 * gm);
-                if (lo > T) {
-                  q = true;
-                } else if (hi <= T) {
-                  q = false;
-                } else {  // ambiguous: the reference's sequential fold (aca.cpp:373-374 / 414-415)
-                  auto cbv = [&](int i) { return col_in_smem ? s_col[gg * m + i] : U[uix(r, i)]; };
-                  double f = hmul(cbv(0), cbv(0));
-                  for (int i = 1; i < m; ++i) f = hadd(f, hmul(cbv(i), cbv(i)));
-                  q = f > T;
-                }
-              }
-            }
-            if (q) {
-              acc = gg;
-              s_prow = gbi;
-              break;
-            }
-            ++consumed;
-          }
-          rejections += consumed;
-          if (acc >= 0) {
-            s_acc = acc;
-            s_next = next + acc;  // accepted column index (advanced after bookkeeping)
-          } else {
-            s_acc = -1;
-            s_next = next + consumed;
-          }
-        }
-        __syncthreads();
-        accepted = s_acc >= 0;
-      }
-      if (!accepted) break;  // no usable column left: converged at rank r (aca.cpp:442-443)
-
-      // ---------------- accepted column: pivot, normalise, pivot-row pass
-      const int ga = s_acc, cstar = s_next, p = s_prow;
-      auto cbv = [&](int i) { return col_in_smem ? s_col[ga * m + i] : U[uix(r, i)]; };
-      if (r == 0 && tid == 0) {
-        // scale2 = exact left fold of the first accepted column (aca.cpp:491)
-        double f = hmul(cbv(0), cbv(0));
-        for (int i = 1; i < m; ++i) f = hadd(f, hmul(cbv(i), cbv(i)));
-        s_scale = f;
-      }
-      const double pivot_val = cbv(p);
-      for (int l = tid; l < r; l += kAcaThreads) s_upiv[l] = U[uix(l, p)];
-      __syncthreads();
-      for (int i = tid; i < m; i += kAcaThreads) U[uix(r, i)] = __ddiv_rn(cbv(i), pivot_val);
-      {
-        double yp[DIM > 0 ? DIM : 20];
-        if constexpr (!DENSE) E.load(rl + p, yp);
-        for (int j = tid; j < n; j += kAcaThreads) {
-          double a;
-          if constexpr (DENSE) a = A[static_cast<long long>(p) * n + j];
-          else a = E.eval(yp, cl + j);
-          const double* vrow = V + static_cast<long long>(j) * kmax;
-          for (int l = 0; l < r; ++l) a = hsub(a, hmul(s_upiv[l], vrow[l]));
-          V[static_cast<long long>(j) * kmax + r] = a;
-        }
-      }
-      if (tid == 0) {
-        s_piv[r] = p;
-        J.row_piv[static_cast<long long>(b) * kmax + r] = p;
-        J.col_piv[static_cast<long long>(b) * kmax + r] = cstar;
-        s_next = cstar + 1;
-      }
-      k_eff = r + 1;
-      __syncthreads();
-      if (J.has_eps) {
-        // epsilon criterion with the reference's exact left folds (aca.cpp:497-538); test path
-        if (tid == 0) {
-          auto ur = [&](int i) { return U[uix(r, i)]; };
-          double nu = hmul(ur(0), ur(0));
-          for (int i = 1; i < m; ++i) nu = hadd(nu, hmul(ur(i), ur(i)));
-          double nv = hmul(V[r], V[r]);
-          for (int j = 1; j < n; ++j) nv = hadd(nv, hmul(V[static_cast<long long>(j) * kmax + r], V[static_cast<long long>(j) * kmax + r]));
-          double cross = 0.0;
-          for (int l = 0; l < r; ++l) {
-            double du = hmul(U[uix(l, 0)], ur(0));
-            for (int i = 1; i < m; ++i) du = hadd(du, hmul(U[uix(l, i)], ur(i)));
-            double dv = hmul(V[l], V[r]);
-            for (int j = 1; j < n; ++j)
-              dv = hadd(dv, hmul(V[static_cast<long long>(j) * kmax + l], V[static_cast<long long>(j) * kmax + r]));
-            cross = hadd(cross, hmul(du, dv));
-          }
-          s_frob = hadd(s_frob, hadd(hmul(2.0, cross), hmul(nu, nv)));
-          const double bound = hmul(J.eps_factor, __dsqrt_rn(s_frob));
-          s_stop = hmul(__dsqrt_rn(nu), __dsqrt_rn(nv)) <= bound ? 1 : 0;
-        }
-        __syncthreads();
-        if (s_stop) break;
-      }
-    }
-    if (tid == 0) {
-      J.k_eff[b] = k_eff;
-      if (J.rejections && rejections) atomicAdd(J.rejections, rejections);
-    }
-    __syncthreads();
-  }
-}
-
-template <int DIM>
-void launch_kernel_aca(const AcaJob& J, const HMatrix& h, cudaStream_t s) {
-  KernelEntry<DIM> E{h.coords.get(), h.n, h.d, h.kp};
-  int occ = 0;
-  HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, aca_kernel<DIM, false>, kAcaThreads, 0));
-  int sms = 0;
-  HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h.device));
-  const long long grid = std::min<long long>(J.njobs, static_cast<long long>(std::max(occ, 1)) * sms);
-  aca_kernel<DIM, false><<<static_cast<unsigned>(std::max(grid, 1ll)), kAcaThreads, 0, s>>>(J, E);
-  HM_LAUNCH_CHECK();
-}
-
-// Team barrier: a warp (NW = 1) or a named barrier over the team's NW warps.
-template <int NW>
-__device__ __forceinline__ void team_sync(int team) {
-  if constexpr (NW == 1) {
-    __syncwarp();
-  } else {
-    asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(NW * 32) : "memory");
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Window kernel: the team kernel's row-in-register layout with a SHARED-memory
-// window of W candidate columns (ring slots col % W, padded stride).  Columns are
-// evaluated W at a time by all threads of the team (fill), their qualification is
-// decided by G = TT/W threads per column (partial sums + the rigorous bound, the
-// reference's sequential fold when ambiguous), and the unconsumed columns stay in
-// the window, receiving each accepted cross as the next step of their chain.  In
-// the noise-floor regime (most columns rejected) this turns the scan
-// into dense, barrier-amortised evaluation.  v_l lives in shared memory (VSM) or
-// directly in the interleaved V factor.
-template <int NW, int KC, int W, bool VSM>
-__host__ __device__ constexpr size_t win_stride() {
-  return static_cast<size_t>(W) * (NW * 64 + 1) + (VSM ? static_cast<size_t>(KC) * NW * 64 : 0) + KC + 2 * NW + W +
-         NW * 64 / 8 + 8;
-}
-
-template <int DIM, int KIND, int NW, int KC, int W, bool VSM, int MINB>
-__global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
-    aca_win_kernel(AcaJob J, KernelEntry<DIM, KIND> E, int teams_per_cta) {
-  constexpr int RPL = 2;
-  constexpr int TT = NW * 32;
-  constexpr int NCAP = TT * RPL;
-  constexpr int PS = NCAP + 1;  // padded slot stride (bank spread for the per-column folds)
-  constexpr int G = TT / W;     // threads per column in the qualification pass
-  static_assert(TT % W == 0 && G >= 1 && (G <= 32 || G % 32 == 0), "window / team shape");
-  constexpr int GL = G < 32 ? G : 32;  // lanes of one column inside a warp
-  constexpr int YD = DIM > 0 ? DIM : 1;
-  extern __shared__ double smem[];
-  const int team = threadIdx.x / TT, t = threadIdx.x % TT, lane = t & 31, wib = t >> 5;
-  if (team >= teams_per_cta) return;
-  double* base = smem + static_cast<size_t>(team) * win_stride<NW, KC, W, VSM>();
-  double* s_win = base;
-  double* s_v = s_win + W * PS;
-  double* s_up = s_v + (VSM ? KC * NCAP : 0);
-  double* s_rbv = s_up + KC;
-  int* s_rbi = reinterpret_cast<int*>(s_rbv + NW);
-  int* s_state = reinterpret_cast<int*>(s_rbv + 2 * NW);
-  unsigned char* s_used = reinterpret_cast<unsigned char*>(s_rbv + 2 * NW + W);
-  double* s_misc = s_rbv + 2 * NW + W + NCAP / 8;  // [0] job, [1] scale, [2] exact-fold verdict
-  const double kEps0sq = 1e-14 * 1e-14;
-  const int kmax = J.kmax;
-  const bool kpow2 = (kmax & (kmax - 1)) == 0;
-  const int kshift = __popc(kmax - 1);
-
-  for (;;) {
-    if (t == 0) s_misc[0] = static_cast<double>(atomicAdd(J.counter, 1));
-    for (int i = t; i < NCAP; i += TT) s_used[i] = 0;
-    team_sync<NW>(team);
-    const long long job = static_cast<long long>(s_misc[0]);
-    team_sync<NW>(team);
-    if (job >= J.njobs) return;
-    const int b = J.order[job];
-    const int rl = J.rl[b], m = J.m[b], cl = J.cl[b], n = J.nn[b];
-    double* U = J.U + (J.u_off[b] - J.u_base);
-    double* V = J.V + (J.v_off[b] - J.v_base);
-    const int tsh = J.tile_shift;
-    auto uix = [&](int l, int i) -> long long {
-      if (tsh < 0) return static_cast<long long>(l) * m + i;
-      return ((static_cast<long long>(i >> tsh) * kmax + l) << tsh) + (i & ((1 << tsh) - 1));
-    };
-    auto vat = [&](int l, int j) -> double& {
-      if constexpr (VSM) return s_v[l * NCAP + j];
-      else return V[static_cast<long long>(j) * kmax + l];
-    };
-
-    double y[RPL][YD];
-    bool rv[RPL];
-#pragma unroll
-    for (int q = 0; q < RPL; ++q) {
-      const int i = t + q * TT;
-      rv[q] = i < m;
-      if constexpr (DIM > 0) {
-#pragma unroll
-        for (int a = 0; a < DIM; ++a) y[q][a] = rv[q] ? __ldg(E.coords + a * E.n + rl + i) : 0.0;
-      }
-    }
-    auto entry = [&](int q, long long colpt) -> double {
-      if constexpr (DIM > 0) {
-        return E.eval(y[q], colpt);
-      } else {
-        double yy[20];
-        E.load(rl + t + q * TT, yy);
-        return E.eval(yy, colpt);
-      }
-    };
-    double uR[RPL][KC];  // right-aligned u_l of the own rows (aca_chain.cuh)
-#pragma unroll
-    for (int q = 0; q < RPL; ++q)
-#pragma unroll
-      for (int j = 0; j < KC; ++j) uR[q][j] = 0.0;
-    int next = 0, filled = 0, k_eff = 0;
-    unsigned long long rejections = 0, ev_col = 0, ev_row = 0;
-    double scale = -1.0;
-    const double gm = static_cast<double>(m) * 1.2e-16;
-
-    for (int r = 0; r < kmax; ++r) {
-      int acc_w = -1;
-      while (next < n) {
-        // speculation depth: while no column was rejected, at most kmax - r more can be
-        // accepted (smooth blocks, d >= 3: no noise floor), so do not evaluate past them
-        const int lim = rejections ? W : max(kmax - r, 1);
-        const int wcols = max(filled, min(min(W, lim), n - next));
-        ev_col += static_cast<unsigned long long>(wcols - filled) * m;
-        // fill: fresh window columns, entry then the reference chain over l < r
-        for (int co = filled; co < wcols; ++co) {
-          const int col = next + co;
-          double* dst = s_win + (col % W) * PS;
-          const double* vb;
-          int vs;
-          if constexpr (VSM) {
-            vb = s_v + static_cast<long long>(r - KC) * NCAP + col;
-            vs = NCAP;
-          } else {
-            vb = V + static_cast<long long>(col) * kmax + (r - KC);
-            vs = 1;
-          }
-          double a0 = rv[0] ? entry(0, cl + col) : 0.0;
-          double a1 = rv[1] ? entry(1, cl + col) : 0.0;
-          Chain<KC>::run2(a0, a1, uR[0], uR[1], r, vb, vs);
-          if (rv[0]) dst[t] = a0;
-          if (rv[1]) dst[t + TT] = a1;
-        }
-        filled = wcols;
-        team_sync<NW>(team);
-        // fast path while the block has rejected nothing (smooth blocks accept the first
-        // candidate of every rank): the first window column with all team threads
-        int first_state = -1;
-        if (rejections == 0) {
-          const double* src = s_win + (next % W) * PS;
-          double sum = 0.0;
-          int nz = 0;
-#pragma unroll
-          for (int q = 0; q < RPL; ++q) {
-            const int i = t + q * TT;
-            if (i < m) {
-              const double a = src[i];
-              sum = hadd(sum, hmul(a, a));
-              nz |= (!s_used[i] && fabs(a) > 0.0) ? 1 : 0;
-            }
-          }
-#pragma unroll
-          for (int o = 16; o; o >>= 1) {
-            sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
-            nz |= __shfl_xor_sync(0xffffffffu, nz, o);
-          }
-          if constexpr (NW > 1) {
-            if (lane == 0) {
-              s_rbv[wib] = sum;
-              s_rbi[wib] = nz;
-            }
-            team_sync<NW>(team);
-            sum = s_rbv[0];
-            nz = s_rbi[0];
-            for (int k2 = 1; k2 < NW; ++k2) {
-              sum = hadd(sum, s_rbv[k2]);
-              nz |= s_rbi[k2];
-            }
-            team_sync<NW>(team);
-          }
-          first_state = 0;
-          if (nz) {
-            if (scale < 0.0) {
-              first_state = 1;
-            } else {
-              const double T = hmul(kEps0sq, scale);
-              const double lo = hmul(sum, 1.0 - 4.0 * gm), hi = hmul(sum, 1.0 + 4.0 * gm);
-              first_state = lo > T ? 1 : (hi <= T ? 0 : 2);
-            }
-          }
-        }
-        if (first_state == 1) {
-          acc_w = 0;
-        } else {
-          // qualification: G threads per column; state 0 no, 1 yes, 2 ambiguous
-          {
-            const int w = t / G, g = t % G;
-            double sum = 0.0;
-            int nz = 0;
-            if (w < wcols) {
-              const double* src = s_win + ((next + w) % W) * PS;
-              for (int i = g; i < m; i += G) {
-                const double a = src[i];
-                sum = hadd(sum, hmul(a, a));
-                nz |= (!s_used[i] && fabs(a) > 0.0) ? 1 : 0;
-              }
-            }
-  #pragma unroll
-            for (int o = GL / 2; o; o >>= 1) {
-              sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
-              nz |= __shfl_xor_sync(0xffffffffu, nz, o);
-            }
-            if constexpr (G > 32) {  // a column spans G/32 warps: combine their partials in warp order
-              if (lane == 0) {
-                s_rbv[wib] = sum;
-                s_rbi[wib] = nz;
-              }
-              team_sync<NW>(team);
-              if (g == 0 && w < wcols) {
-                sum = s_rbv[wib];
-                nz = s_rbi[wib];
-                for (int k2 = 1; k2 < G / 32; ++k2) {
-                  sum = hadd(sum, s_rbv[wib + k2]);
-                  nz |= s_rbi[wib + k2];
-                }
-              }
-            }
-            if (g == 0 && w < wcols) {
-              int st = 0;
-              if (nz) {
-                if (scale < 0.0) {
-                  st = 1;
-                } else {
-                  const double T = hmul(kEps0sq, scale);
-                  const double lo = hmul(sum, 1.0 - 4.0 * gm), hi = hmul(sum, 1.0 + 4.0 * gm);
-                  st = lo > T ? 1 : (hi <= T ? 0 : 2);
-                }
-              }
-              s_state[w] = st;
-            }
-          }
-          team_sync<NW>(team);
-          for (int w = 0; w < wcols; ++w) {
-            int st = s_state[w];
-            if (st == 2) {  // the reference's sequential left fold (aca.cpp:373-374 / 414-415)
-              if (t == 0) {
-                const double* src = s_win + ((next + w) % W) * PS;
-                double f = hmul(src[0], src[0]);
-                for (int i = 1; i < m; ++i) f = hadd(f, hmul(src[i], src[i]));
-                s_misc[2] = f > hmul(kEps0sq, scale) ? 1.0 : 0.0;
-              }
-              team_sync<NW>(team);
-              st = s_misc[2] != 0.0 ? 1 : 0;
-              team_sync<NW>(team);
-            }
-            if (st == 1) {
-              acc_w = w;
-              break;
-            }
-          }
-        }
-        const int consumed = acc_w >= 0 ? acc_w + 1 : wcols;
-        rejections += static_cast<unsigned long long>(acc_w >= 0 ? acc_w : wcols);
-        next += consumed;
-        filled = acc_w >= 0 ? wcols - consumed : 0;
-        if (acc_w >= 0) break;
-      }
-      if (acc_w < 0) break;  // no usable column left (aca.cpp:442-443)
-      const int cstar = next - 1;
-      const double* acol = s_win + (cstar % W) * PS;
-
-      // pivot row: argmax |u_hat| over unused rows, first index wins (aca.cpp:367, 375-376)
-      double bv = -1.0;
-      int bi = 0x7fffffff;
-#pragma unroll
-      for (int q = 0; q < RPL; ++q) {
-        const int i = t + q * TT;
-        if (rv[q] && !s_used[i]) {
-          const double av = fabs(acol[i]);
-          if (av > bv) {
-            bv = av;
-            bi = i;
-          }
-        }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        argmax_combine(bv, bi, ov, oi);
-      }
-      if constexpr (NW > 1) {
-        if (lane == 0) {
-          s_rbv[wib] = bv;
-          s_rbi[wib] = bi;
-        }
-        team_sync<NW>(team);
-        bv = s_rbv[0];
-        bi = s_rbi[0];
-        for (int g = 1; g < NW; ++g) argmax_combine(bv, bi, s_rbv[g], s_rbi[g]);
-      }
-      const int p = bi;
-      if (r == 0 && t == 0) {  // scale2 = exact left fold of the first accepted column (aca.cpp:491)
-        double f = hmul(acol[0], acol[0]);
-        for (int i = 1; i < m; ++i) f = hadd(f, hmul(acol[i], acol[i]));
-        s_misc[1] = f;
-      }
-      const int pt = p % TT, pq = p / TT;
-      if (t == pt) {
-#pragma unroll
-        for (int q = 0; q < RPL; ++q) {
-          if (q == pq) {
-#pragma unroll
-            for (int j = 0; j < KC; ++j)
-              if (j >= KC - r) s_up[j - (KC - r)] = uR[q][j];
-          }
-        }
-      }
-      team_sync<NW>(team);
-      if (r == 0) scale = s_misc[1];
-      const double pivot_val = acol[p];
-      // u_r = u_hat / pivot (aca.cpp:466-470), appended right-aligned
-#pragma unroll
-      for (int q = 0; q < RPL; ++q) {
-        const double nu = rv[q] ? __ddiv_rn(acol[t + q * TT], pivot_val) : 0.0;
-#pragma unroll
-        for (int j = 0; j + 1 < KC; ++j) uR[q][j] = uR[q][j + 1];
-        uR[q][KC - 1] = nu;
-      }
-      // v_r = A(p,:) - sum_l u_l[p] v_l (aca.cpp:474-481); window columns already hold it
-      ev_row += n;
-      {
-        double yp[DIM > 0 ? DIM : 20];
-        E.load(rl + p, yp);
-        double uP[KC];  // u_l[p], right-aligned (aca_chain.cuh)
-#pragma unroll
-        for (int j = 0; j < KC; ++j) uP[j] = j >= KC - r ? s_up[j - (KC - r)] : 0.0;
-        for (int j = t; j < n; j += TT) {
-          double a;
-          if (j >= next && j < next + filled) {
-            a = s_win[(j % W) * PS + p];
-          } else {
-            const double* vb;
-            int vs;
-            if constexpr (VSM) {
-              vb = s_v + static_cast<long long>(r - KC) * NCAP + j;
-              vs = NCAP;
-            } else {
-              vb = V + static_cast<long long>(j) * kmax + (r - KC);
-              vs = 1;
-            }
-            a = Chain<KC>::run(E.eval(yp, cl + j), uP, r, vb, vs);
-          }
-          vat(r, j) = a;
-        }
-      }
-      team_sync<NW>(team);
-      if (t == pt) s_used[p] = 1;  // after every reader of the old flag (argmax above)
-      // window columns receive this cross (next step of their chain)
-      for (int co = 0; co < filled; ++co) {
-        const int col = next + co;
-        const double vr = vat(r, col);
-        double* dst = s_win + (col % W) * PS;
-#pragma unroll
-        for (int q = 0; q < RPL; ++q)
-          if (rv[q]) dst[t + q * TT] = hsub(dst[t + q * TT], hmul(uR[q][KC - 1], vr));
-      }
-      if (t == 0) {
-        J.row_piv[static_cast<long long>(b) * kmax + r] = p;
-        J.col_piv[static_cast<long long>(b) * kmax + r] = cstar;
-      }
-      k_eff = r + 1;
-    }
-    // factors: U (layout uix), V interleaved n x kmax, zero past k_eff
-#pragma unroll
-    for (int j = 0; j < KC; ++j) {
-      const int l = j - (KC - k_eff);
-      if (l >= 0) {
-#pragma unroll
-        for (int q = 0; q < RPL; ++q)
-          if (rv[q]) U[uix(l, t + q * TT)] = uR[q][j];
-      }
-    }
-    for (int l = k_eff; l < kmax; ++l)
-#pragma unroll
-      for (int q = 0; q < RPL; ++q)
-        if (rv[q]) U[uix(l, t + q * TT)] = 0.0;
-    if constexpr (VSM) {
-      team_sync<NW>(team);
-      for (int idx = t; idx < n * kmax; idx += TT) {
-        // kmax is a power of two in practice (k = 16): shift instead of an integer division
-        const int j = kpow2 ? idx >> kshift : idx / kmax, l = idx - j * kmax;
-        V[idx] = l < k_eff ? s_v[l * NCAP + j] : 0.0;
-      }
-    } else {
-      for (int idx = t; idx < n * (kmax - k_eff); idx += TT) {
-        const int j = idx / (kmax - k_eff), l = k_eff + idx % (kmax - k_eff);
-        V[static_cast<long long>(j) * kmax + l] = 0.0;
-      }
-    }
-    for (int l = k_eff + t; l < kmax; l += TT) {
-      J.row_piv[static_cast<long long>(b) * kmax + l] = -1;
-      J.col_piv[static_cast<long long>(b) * kmax + l] = -1;
-    }
-    if (t == 0) {
-      J.k_eff[b] = k_eff;
-      if (J.rejections && rejections) atomicAdd(J.rejections, rejections);
-      if (J.evals) {
-        atomicAdd(J.evals, ev_col);
-        atomicAdd(J.evals + 1, ev_row);
-        atomicAdd(J.evals + 2, 1ull);
-      }
-    }
-    team_sync<NW>(team);
-  }
-}
-
-template <int DIM, int KIND, int NW, int KC, int W, bool VSM, int MINB = 1>
-void launch_win(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, cudaStream_t s) {
-  if (J.njobs <= 0) return;
-  constexpr int teams = NW >= 4 ? 1 : 4 / NW;
-  const size_t smem = teams * win_stride<NW, KC, W, VSM>() * sizeof(double);
-  auto kfn = aca_win_kernel<DIM, KIND, NW, KC, W, VSM, MINB>;
-  HM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  int occ = 0;
-  HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, teams * NW * 32, smem));
-  const long long ctas = std::min<long long>((J.njobs + teams - 1) / teams, static_cast<long long>(std::max(occ, 1)) * sms);
-  kfn<<<static_cast<unsigned>(std::max(ctas, 1ll)), teams * NW * 32, smem, s>>>(J, E, teams);
-  HM_LAUNCH_CHECK();
-}
-
-// ---------------------------------------------------------------------------
-// Big-block kernel (max(m, n) > 1024): one 256-thread CTA per block, rows strided
-// over the CTA in pairs.  The window of W candidate columns lives in a per-CTA
-// global scratch (L2-resident: W x m doubles); for each row pair a thread loads
-// u_l of its two rows from the U factor into right-aligned registers once and
-// reuses them for every fresh window column (Chain<KC>::run2), so the chain costs
-// one broadcast v load per step as in the window kernels.  Pivot rows are a
-// shared bitmask.  Same semantics and bits as the window kernels.
-constexpr int kBigThreads = 256;
-constexpr int kBigW = 8;
-
-template <int DIM, int KIND, int KC>
-__global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, KernelEntry<DIM, KIND> E, double* gscratch,
-                                                              long long gstride, int mask_words) {
-  constexpr int TT = kBigThreads;
-  constexpr int W = kBigW;
-  constexpr int G = TT / W;  // 32: one warp per column in the qualification pass
-  constexpr int YD = DIM > 0 ? DIM : 20;
-  extern __shared__ double smem[];
-  unsigned* s_mask = reinterpret_cast<unsigned*>(smem);
-  double* s_up = smem + (mask_words + 1) / 2;  // kKmax
-  double* s_rbv = s_up + kKmax;                // 8 warps
-  int* s_rbi = reinterpret_cast<int*>(s_rbv + 8);
-  int* s_state = reinterpret_cast<int*>(s_rbv + 12);
-  double* s_misc = s_rbv + 20;  // [0] job [1] scale [2] verdict
-  const int t = threadIdx.x, lane = t & 31, wib = t >> 5;
-  const double kEps0sq = 1e-14 * 1e-14;
-  const int kmax = J.kmax;
-  double* win = gscratch + static_cast<long long>(blockIdx.x) * gstride * W;
-
-  for (;;) {
-    if (t == 0) s_misc[0] = static_cast<double>(atomicAdd(J.counter, 1));
-    __syncthreads();
-    const long long job = static_cast<long long>(s_misc[0]);
-    if (job >= J.njobs) return;
-    const int b = J.order[job];
-    const int rl = J.rl[b], m = J.m[b], cl = J.cl[b], n = J.nn[b];
-    double* U = J.U + (J.u_off[b] - J.u_base);
-    double* V = J.V + (J.v_off[b] - J.v_base);
-    const int tsh = J.tile_shift;
-    auto uix = [&](int l, int i) -> long long {
-      if (tsh < 0) return static_cast<long long>(l) * m + i;
-      return ((static_cast<long long>(i >> tsh) * kmax + l) << tsh) + (i & ((1 << tsh) - 1));
-    };
-    const long long PS = gstride;
-    for (int i = t; i < (m + 31) / 32; i += TT) s_mask[i] = 0u;
-    __syncthreads();
-    auto is_used = [&](int i) -> bool { return (s_mask[i >> 5] >> (i & 31)) & 1u; };
-
-    int next = 0, filled = 0, k_eff = 0;
-    unsigned long long rejections = 0, ev_col = 0, ev_row = 0;
-    double scale = -1.0;
-    const double gm = static_cast<double>(m) * 1.2e-16;
-
-    for (int r = 0; r < kmax; ++r) {
-      int acc_w = -1;
-      while (next < n) {
-        // speculation depth: while no column was rejected, at most kmax - r more can be
-        // accepted (smooth blocks, d >= 3: no noise floor), so do not evaluate past them
-        const int lim = rejections ? W : max(kmax - r, 1);
-        const int wcols = max(filled, min(min(W, lim), n - next));
-        ev_col += static_cast<unsigned long long>(wcols - filled) * m;
-        // fill: per row pair, u of the two rows into registers once, then every fresh column
-        for (int i0 = t; i0 < m; i0 += 2 * TT) {
-          const int i1 = i0 + TT;
-          const bool ok1 = i1 < m;
-          double uR[2][KC];
-#pragma unroll
-          for (int j = 0; j < KC; ++j) {
-            const int l = j - (KC - r);
-            uR[0][j] = l >= 0 ? U[uix(l, i0)] : 0.0;
-            uR[1][j] = (l >= 0 && ok1) ? U[uix(l, i1)] : 0.0;
-          }
-          double y0[YD], y1[YD];
-          E.load(rl + i0, y0);
-          E.load(rl + (ok1 ? i1 : i0), y1);
-          for (int co = filled; co < wcols; ++co) {
-            const int col = next + co;
-            double a0 = E.eval(y0, cl + col);
-            double a1 = ok1 ? E.eval(y1, cl + col) : 0.0;
-            Chain<KC>::run2(a0, a1, uR[0], uR[1], r, V + static_cast<long long>(col) * kmax + (r - KC), 1);
-            double* dst = win + static_cast<long long>(col % W) * PS;
-            dst[i0] = a0;
-            if (ok1) dst[i1] = a1;
-          }
-        }
-        filled = wcols;
-        __syncthreads();
-        {
-          const int w = wib;  // G == 32: warp w scans window column w
-          double sum = 0.0;
-          int nz = 0;
-          if (w < wcols) {
-            const double* src = win + static_cast<long long>((next + w) % W) * PS;
-            for (int i = lane; i < m; i += 32) {
-              const double a = src[i];
-              sum = hadd(sum, hmul(a, a));
-              nz |= (!is_used(i) && fabs(a) > 0.0) ? 1 : 0;
-            }
-          }
-#pragma unroll
-          for (int o = 16; o; o >>= 1) {
-            sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
-            nz |= __shfl_xor_sync(0xffffffffu, nz, o);
-          }
-          if (lane == 0 && w < wcols) {
-            int st = 0;
-            if (nz) {
-              if (scale < 0.0) {
-                st = 1;
-              } else {
-                const double T = hmul(kEps0sq, scale);
-                const double lo = hmul(sum, 1.0 - 4.0 * gm), hi = hmul(sum, 1.0 + 4.0 * gm);
-                st = lo > T ? 1 : (hi <= T ? 0 : 2);
-              }
-            }
-            s_state[w] = st;
-          }
-        }
-        __syncthreads();
-        for (int w = 0; w < wcols; ++w) {
-          int st = s_state[w];
-          if (st == 2) {
-            if (t == 0) {
-              const double* src = win + static_cast<long long>((next + w) % W) * PS;
-              double f = hmul(src[0], src[0]);
-              for (int i = 1; i < m; ++i) f = hadd(f, hmul(src[i], src[i]));
-              s_misc[2] = f > hmul(kEps0sq, scale) ? 1.0 : 0.0;
-            }
-            __syncthreads();
-            st = s_misc[2] != 0.0 ? 1 : 0;
-            __syncthreads();
-          }
-          if (st == 1) {
-            acc_w = w;
-            break;
-          }
-        }
-        const int consumed = acc_w >= 0 ? acc_w + 1 : wcols;
-        rejections += static_cast<unsigned long long>(acc_w >= 0 ? acc_w : wcols);
-        next += consumed;
-        filled = acc_w >= 0 ? wcols - consumed : 0;
-        if (acc_w >= 0) break;
-      }
-      if (acc_w < 0) break;
-      const int cstar = next - 1;
-      const double* acol = win + static_cast<long long>(cstar % W) * PS;
-      double bv = -1.0;
-      int bi = 0x7fffffff;
-      for (int i = t; i < m; i += TT) {
-        if (!is_used(i)) {
-          const double av = fabs(acol[i]);
-          if (av > bv) {
-            bv = av;
-            bi = i;
-          }
-        }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        argmax_combine(bv, bi, ov, oi);
-      }
-      if (lane == 0) {
-        s_rbv[wib] = bv;
-        s_rbi[wib] = bi;
-      }
-      __syncthreads();
-      bv = s_rbv[0];
-      bi = s_rbi[0];
-      for (int g = 1; g < TT / 32; ++g) argmax_combine(bv, bi, s_rbv[g], s_rbi[g]);
-      const int p = bi;
-      if (t == 0) {
-        if (r == 0) {
-          double f = hmul(acol[0], acol[0]);
-          for (int i = 1; i < m; ++i) f = hadd(f, hmul(acol[i], acol[i]));
-          s_misc[1] = f;
-        }
-        for (int l = 0; l < r; ++l) s_up[l] = U[uix(l, p)];
-      }
-      __syncthreads();
-      if (r == 0) scale = s_misc[1];
-      const double pivot_val = acol[p];
-      for (int i = t; i < m; i += TT) U[uix(r, i)] = __ddiv_rn(acol[i], pivot_val);
-      ev_row += n;
-      {
-        double yp[YD];
-        E.load(rl + p, yp);
-        double uP[KC];  // u_l[p], right-aligned: every V-row load of the chain issues up front
-#pragma unroll
-        for (int j = 0; j < KC; ++j) uP[j] = j >= KC - r ? s_up[j - (KC - r)] : 0.0;
-        for (int j = t; j < n; j += TT) {
-          double a;
-          if (j >= next && j < next + filled) {
-            a = win[static_cast<long long>(j % W) * PS + p];
-          } else {
-            a = Chain<KC>::run(E.eval(yp, cl + j), uP, r, V + static_cast<long long>(j) * kmax + (r - KC), 1);
-          }
-          V[static_cast<long long>(j) * kmax + r] = a;
-        }
-      }
-      __syncthreads();
-      if (t == 0) s_mask[p >> 5] |= 1u << (p & 31);
-      for (int co = 0; co < filled; ++co) {
-        const int col = next + co;
-        const double vr = V[static_cast<long long>(col) * kmax + r];
-        double* dst = win + static_cast<long long>(col % W) * PS;
-        for (int i = t; i < m; i += TT) dst[i] = hsub(dst[i], hmul(U[uix(r, i)], vr));
-      }
-      if (t == 0) {
-        J.row_piv[static_cast<long long>(b) * kmax + r] = p;
-        J.col_piv[static_cast<long long>(b) * kmax + r] = cstar;
-      }
-      k_eff = r + 1;
-    }
-    for (int l = k_eff; l < kmax; ++l)
-      for (int i = t; i < m; i += TT) U[uix(l, i)] = 0.0;
-    if (k_eff < kmax) {
-      for (int idx = t; idx < n * (kmax - k_eff); idx += TT) {
-        const int j = idx / (kmax - k_eff), l = k_eff + idx % (kmax - k_eff);
-        V[static_cast<long long>(j) * kmax + l] = 0.0;
-      }
-    }
-    for (int l = k_eff + t; l < kmax; l += TT) {
-      J.row_piv[static_cast<long long>(b) * kmax + l] = -1;
-      J.col_piv[static_cast<long long>(b) * kmax + l] = -1;
-    }
-    if (t == 0) {
-      J.k_eff[b] = k_eff;
-      if (J.rejections && rejections) atomicAdd(J.rejections, rejections);
-      if (J.evals) {
-        atomicAdd(J.evals, ev_col);
-        atomicAdd(J.evals + 1, ev_row);
-        atomicAdd(J.evals + 2, 1ull);
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Cluster kernel (1024 < max(m, n) <= 512 * CL): a THREAD-BLOCK CLUSTER of CL CTAs
-// (256 threads each) factorises one block.  CTA c of the cluster owns rows
-// [512c, 512c + 512) with u_l right-aligned in registers (exactly the window kernel's
-// thread mapping) and keeps its rows of the W-column window in its own shared memory.
-// Per-column partial norms, the pivot argmax, the exact folds and the pivot row's u_l
-// travel through distributed shared memory (mapa / ld.shared::cluster via
-// cluster.map_shared_rank); every CTA combines the CL partials in rank order, so all
-// CTAs take identical decisions and the whole factorisation is bitwise the reference's.
-// v_l lives in the interleaved V factor (written by the row pass, made visible to the
-// cluster by the release/acquire cluster barrier).
-template <int DIM, int KIND, int KC, int CL>
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
-    aca_cluster_kernel(AcaJob J, KernelEntry<DIM, KIND> E) {
-  namespace cg = cooperative_groups;
-  constexpr int TT = 256, RPL = 2, NCAP = TT * RPL, W = 16, PS = NCAP + 1, G = TT / W;  // G = 16
-  constexpr int YD = DIM > 0 ? DIM : 1;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int cr = static_cast<int>(cluster.block_rank());
-  extern __shared__ double smem[];
-  double* s_win = smem;                       // W x PS (own rows)
-  double* s_up = s_win + W * PS;              // KC: u_l[p] (copied from the owner)
-  double* s_csum = s_up + KC;                 // W: this CTA's partial norm per column
-  int* s_cnz = reinterpret_cast<int*>(s_csum + W);      // W ints
-  double* s_wsum = s_csum + W + W / 2;        // 8 warps x 2 (sum pieces for G=16 groups)
-  double* s_rbv = s_wsum + 16;                // 8 warps (argmax)
-  int* s_rbi = reinterpret_cast<int*>(s_rbv + 8);       // 8 ints
-  double* s_cbv = s_rbv + 12;                 // [0] CTA argmax value, [1] (int) index
-  int* s_state = reinterpret_cast<int*>(s_cbv + 2);     // W ints
-  unsigned char* s_used = reinterpret_cast<unsigned char*>(s_cbv + 2 + W / 2);  // NCAP bytes
-  double* s_misc = s_cbv + 2 + W / 2 + NCAP / 8;  // [0] job [1] scale [2] verdict [3] pivot value
-  double* s_tot = s_misc + 8;                     // W: combined norm per window column
-  double* s_scr = s_tot + W;                      // NCAP: re-evaluated first column (exact scale2)
-  const int t = threadIdx.x, lane = t & 31, wib = t >> 5;
-  const double kEps0sq = 1e-14 * 1e-14;
-  const int kmax = J.kmax;
-  auto rem = [&](double* p, int rank) -> const double* { return cluster.map_shared_rank(p, rank); };
-
-  for (;;) {
-    if (cr == 0 && t == 0) s_misc[0] = static_cast<double>(atomicAdd(J.counter, 1));
-    for (int i = t; i < NCAP; i += TT) s_used[i] = 0;
-    cluster.sync();
-    const long long job = static_cast<long long>(*rem(s_misc, 0));
-    cluster.sync();  // everyone has read the job before rank 0 may overwrite it
-    if (job >= J.njobs) return;
-    const int b = J.order[job];
-    const int rl = J.rl[b], m = J.m[b], cl = J.cl[b], n = J.nn[b];
-    double* U = J.U + (J.u_off[b] - J.u_base);
-    double* V = J.V + (J.v_off[b] - J.v_base);
-    const int tsh = J.tile_shift;
-    auto uix = [&](int l, int i) -> long long {
-      if (tsh < 0) return static_cast<long long>(l) * m + i;
-      return ((static_cast<long long>(i >> tsh) * kmax + l) << tsh) + (i & ((1 << tsh) - 1));
-    };
-    const int row0 = cr * NCAP;  // first block row of this CTA
-    double y[RPL][YD];
-    bool rv[RPL];
-#pragma unroll
-    for (int q = 0; q < RPL; ++q) {
-      const int i = row0 + t + q * TT;
-      rv[q] = i < m;
-      if constexpr (DIM > 0) {
-#pragma unroll
-        for (int a = 0; a < DIM; ++a) y[q][a] = rv[q] ? __ldg(E.coords + a * E.n + rl + i) : 0.0;
-      }
-    }
-    auto entry = [&](int q, long long colpt) -> double {
-      if constexpr (DIM > 0) {
-        return E.eval(y[q], colpt);
-      } else {
-        double yy[20];
-        E.load(rl + row0 + t + q * TT, yy);
-        return E.eval(yy, colpt);
-      }
-    };
-    double uR[RPL][KC];
-#pragma unroll
-    for (int q = 0; q < RPL; ++q)
-#pragma unroll
-      for (int j = 0; j < KC; ++j) uR[q][j] = 0.0;
-    int next = 0, filled = 0, k_eff = 0;
-    unsigned long long rejections = 0, ev_col = 0, ev_row = 0;
-    double scale = -1.0, s_lo = 0.0, s_hi = 0.0;  // scale2: exact (scale_exact) or bracket
-    bool have_scale = false, scale_exact = false;
-    int c0col = 0;
-    const double gm = static_cast<double>(m) * 1.2e-16;
-    // exact left fold of a window column over ALL rows (rank order, then row order)
-    auto exact_fold = [&](int slot) -> double {
-      double f = 0.0;
-      bool first = true;
-      for (int c = 0; c < CL; ++c) {
-        const double* w = rem(s_win, c) + slot * PS;
-        const int rows = min(NCAP, m - c * NCAP);
-        for (int i = 0; i < rows; ++i) {
-          const double a = w[i];
-          f = first ? hmul(a, a) : hadd(f, hmul(a, a));
-          first = false;
-        }
-      }
-      return f;
-    };
-
-    for (int r = 0; r < kmax; ++r) {
-      int acc_w = -1;
-      while (next < n) {
-        const int lim = rejections ? W : max(kmax - r, 1);
-        const int wcols = max(filled, min(min(W, lim), n - next));
-        ev_col += static_cast<unsigned long long>(wcols - filled) * m;
-        for (int co = filled; co < wcols; ++co) {
-          const int col = next + co;
-          double* dst = s_win + (col % W) * PS;
-          double a0 = rv[0] ? entry(0, cl + col) : 0.0;
-          double a1 = rv[1] ? entry(1, cl + col) : 0.0;
-          Chain<KC>::run2(a0, a1, uR[0], uR[1], r, V + static_cast<long long>(col) * kmax + (r - KC), 1);
-          if (rv[0]) dst[t] = a0;
-          if (rv[1]) dst[t + TT] = a1;
-        }
-        filled = wcols;
-        __syncthreads();
-        // this CTA's partial norm / nonzero flag per window column (G = 16 threads each)
-        {
-          const int w = t / G, g = t % G;
-          double sum = 0.0;
-          int nz = 0;
-          if (w < wcols) {
-            const double* src = s_win + ((next + w) % W) * PS;
-            const int rows = min(NCAP, m - row0);
-            for (int i = g; i < rows; i += G) {
-              const double a = src[i];
-              sum = hadd(sum, hmul(a, a));
-              nz |= (!s_used[i] && fabs(a) > 0.0) ? 1 : 0;
-            }
-          }
-#pragma unroll
-          for (int o = G / 2; o; o >>= 1) {
-            sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
-            nz |= __shfl_xor_sync(0xffffffffu, nz, o);
-          }
-          if (g == 0) {
-            s_csum[w] = sum;
-            s_cnz[w] = nz;
-          }
-        }
-        cluster.sync();
-        // identical decision in every CTA: partials combined in rank order.  scale2 is
-        // known exactly only on demand (see scale_exact): until then the test uses the
-        // bracket [s_lo, s_hi] of the parallel sum, which contains the exact left fold.
-        if (t < W) {
-          const int w = t;
-          int st = 0;
-          double sum = 0.0;
-          if (w < wcols) {
-            double ps[CL];
-            int pn[CL];
-#pragma unroll
-            for (int c = 0; c < CL; ++c) {  // all remote loads issued before the fold
-              ps[c] = *rem(s_csum + w, c);
-              pn[c] = cluster.map_shared_rank(s_cnz, c)[w];
-            }
-            int nz = 0;
-            sum = ps[0];
-#pragma unroll
-            for (int c = 0; c < CL; ++c) {
-              if (c) sum = hadd(sum, ps[c]);
-              nz |= pn[c];
-            }
-            if (nz) {
-              if (!have_scale) {
-                st = 1;
-              } else {
-                const double Tlo = hmul(kEps0sq, scale_exact ? scale : s_lo);
-                const double Thi = hmul(kEps0sq, scale_exact ? scale : s_hi);
-                const double lo = hmul(sum, 1.0 - 4.0 * gm), hi = hmul(sum, 1.0 + 4.0 * gm);
-                st = lo > Thi ? 1 : (hi <= Tlo ? 0 : 2);
-              }
-            }
-          }
-          s_state[w] = st;
-          s_tot[w] = sum;
-        }
-        __syncthreads();
-        for (int w = 0; w < wcols; ++w) {
-          int st = s_state[w];
-          if (st == 2) {  // the reference's sequential left folds (aca.cpp:373-374, 491)
-            if (!scale_exact) {
-              // the first accepted column is A(:, c0col) (no cross subtracted yet):
-              // re-evaluate it (bitwise the same entries) and fold it over all rows
-#pragma unroll
-              for (int q = 0; q < RPL; ++q)
-                if (rv[q]) s_scr[t + q * TT] = entry(q, cl + c0col);
-              cluster.sync();
-              if (t == 0) {
-                double f = 0.0;
-                bool first = true;
-                for (int c = 0; c < CL; ++c) {
-                  const double* w2 = rem(s_scr, c);
-                  const int rows = min(NCAP, m - c * NCAP);
-                  for (int i = 0; i < rows; ++i) {
-                    f = first ? hmul(w2[i], w2[i]) : hadd(f, hmul(w2[i], w2[i]));
-                    first = false;
-                  }
-                }
-                s_misc[1] = f;
-              }
-              cluster.sync();
-              scale = s_misc[1];
-              scale_exact = true;
-            }
-            if (t == 0) s_misc[2] = exact_fold((next + w) % W) > hmul(kEps0sq, scale) ? 1.0 : 0.0;
-            __syncthreads();
-            st = s_misc[2] != 0.0 ? 1 : 0;
-          }
-          if (st == 1) {
-            acc_w = w;
-            break;
-          }
-        }
-        if (!have_scale && acc_w >= 0) {
-          // first cross: bracket of scale2 from the parallel norm of the accepted column
-          const double sp = s_tot[acc_w];
-          s_lo = hmul(sp, 1.0 - 4.0 * gm);
-          s_hi = hmul(sp, 1.0 + 4.0 * gm);
-          c0col = next + acc_w;
-          have_scale = true;
-        }
-        cluster.sync();  // partials / windows read by every CTA before they change
-        const int consumed = acc_w >= 0 ? acc_w + 1 : wcols;
-        rejections += static_cast<unsigned long long>(acc_w >= 0 ? acc_w : wcols);
-        next += consumed;
-        filled = acc_w >= 0 ? wcols - consumed : 0;
-        if (acc_w >= 0) break;
-      }
-      if (acc_w < 0) break;  // no usable column left (aca.cpp:442-443)
-      const int cstar = next - 1;
-      const int aslot = cstar % W;
-      const double* acol = s_win + aslot * PS;
-
-      // pivot row: argmax over unused rows, first (global) index wins
-      double bv = -1.0;
-      int bi = 0x7fffffff;
-#pragma unroll
-      for (int q = 0; q < RPL; ++q) {
-        const int il = t + q * TT;
-        if (rv[q] && !s_used[il]) {
-          const double av = fabs(acol[il]);
-          if (av > bv) {
-            bv = av;
-            bi = row0 + il;
-          }
-        }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        argmax_combine(bv, bi, ov, oi);
-      }
-      if (lane == 0) {
-        s_rbv[wib] = bv;
-        s_rbi[wib] = bi;
-      }
-      __syncthreads();
-      if (t == 0) {
-        double cbv = s_rbv[0];
-        int cbi = s_rbi[0];
-        for (int g = 1; g < TT / 32; ++g) argmax_combine(cbv, cbi, s_rbv[g], s_rbi[g]);
-        s_cbv[0] = cbv;
-        reinterpret_cast<int*>(s_cbv + 1)[0] = cbi;
-      }
-      cluster.sync();
-      int p;
-      {
-        double gbv = -1.0;
-        int gbi = 0x7fffffff;
-        double cv[CL];
-        int ci[CL];
-#pragma unroll
-        for (int c = 0; c < CL; ++c) {
-          const double* rc = rem(s_cbv, c);
-          cv[c] = rc[0];
-          ci[c] = reinterpret_cast<const int*>(rc + 1)[0];
-        }
-#pragma unroll
-        for (int c = 0; c < CL; ++c) argmax_combine(gbv, gbi, cv[c], ci[c]);
-        p = gbi;
-      }
-      const int po = p / NCAP, pl = p - po * NCAP, pt = pl % TT, pq = pl / TT;
-      if (cr == po && t == pt) {
-#pragma unroll
-        for (int q = 0; q < RPL; ++q) {
-          if (q == pq) {
-            s_misc[3] = acol[pl];
-#pragma unroll
-            for (int j = 0; j < KC; ++j)
-              if (j >= KC - r) s_up[j - (KC - r)] = uR[q][j];
-          }
-        }
-      }
-      cluster.sync();
-      // the owner's u_l[p] and pivot value into every CTA
-      if (cr != po) {
-        const double* ru = rem(s_up, po);
-        for (int l = t; l < r; l += TT) s_up[l] = ru[l];
-        if (t == 0) s_misc[3] = *rem(s_misc + 3, po);
-      }
-      __syncthreads();
-      const double pivot_val = s_misc[3];
-#pragma unroll
-      for (int q = 0; q < RPL; ++q) {
-        const double nu = rv[q] ? __ddiv_rn(acol[t + q * TT], pivot_val) : 0.0;
-#pragma unroll
-        for (int j = 0; j + 1 < KC; ++j) uR[q][j] = uR[q][j + 1];
-        uR[q][KC - 1] = nu;
-      }
-      // v_r = A(p,:) - sum_l u_l[p] v_l (aca.cpp:474-481), columns split over the cluster
-      ev_row += n;
-      {
-        double yp[DIM > 0 ? DIM : 20];
-        E.load(rl + p, yp);
-        double uP[KC];
-#pragma unroll
-        for (int j = 0; j < KC; ++j) uP[j] = j >= KC - r ? s_up[j - (KC - r)] : 0.0;
-        for (int j = cr * TT + t; j < n; j += CL * TT)
-          V[static_cast<long long>(j) * kmax + r] =
-              Chain<KC>::run(E.eval(yp, cl + j), uP, r, V + static_cast<long long>(j) * kmax + (r - KC), 1);
-      }
-      cluster.sync();  // v_r visible to the whole cluster (release / acquire)
-      if (cr == po && t == pt) s_used[pl] = 1;
-      for (int co = 0; co < filled; ++co) {
-        const int col = next + co;
-        const double vr = V[static_cast<long long>(col) * kmax + r];
-        double* dst = s_win + (col % W) * PS;
-#pragma unroll
-        for (int q = 0; q < RPL; ++q)
-          if (rv[q]) dst[t + q * TT] = hsub(dst[t + q * TT], hmul(uR[q][KC - 1], vr));
-      }
-      if (cr == 0 && t == 0) {
-        J.row_piv[static_cast<long long>(b) * kmax + r] = p;
-        J.col_piv[static_cast<long long>(b) * kmax + r] = cstar;
-      }
-      k_eff = r + 1;
-      __syncthreads();
-    }
-    // factors: own rows of U; V past k_eff zeroed (columns split over the cluster)
-#pragma unroll
-    for (int j = 0; j < KC; ++j) {
-      const int l = j - (KC - k_eff);
-      if (l >= 0) {
-#pragma unroll
-        for (int q = 0; q < RPL; ++q)
-          if (rv[q]) U[uix(l, row0 + t + q * TT)] = uR[q][j];
-      }
-    }
-    for (int l = k_eff; l < kmax; ++l)
-#pragma unroll
-      for (int q = 0; q < RPL; ++q)
-        if (rv[q]) U[uix(l, row0 + t + q * TT)] = 0.0;
-    if (k_eff < kmax)
-      for (int j = cr * TT + t; j < n; j += CL * TT)
-        for (int l = k_eff; l < kmax; ++l) V[static_cast<long long>(j) * kmax + l] = 0.0;
-    if (cr == 0) {
-      for (int l = k_eff + t; l < kmax; l += TT) {
-        J.row_piv[static_cast<long long>(b) * kmax + l] = -1;
-        J.col_piv[static_cast<long long>(b) * kmax + l] = -1;
-      }
-      if (t == 0) {
-        J.k_eff[b] = k_eff;
-        if (J.rejections && rejections) atomicAdd(J.rejections, rejections);
-        if (J.evals) {
-          atomicAdd(J.evals, ev_col);
-          atomicAdd(J.evals + 1, ev_row);
-          atomicAdd(J.evals + 2, 1ull);
-        }
-      }
-    }
-    cluster.sync();
-  }
-}
-
-template <int DIM, int KIND, int KC, int CL>
-void launch_cluster(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, cudaStream_t s) {
-  if (J.njobs <= 0) return;
-  constexpr int W = 16, NCAP = 512;
-  const size_t smem = sizeof(double) * (W * (NCAP + 1) + KC + W + W / 2 + 16 + 12 + 2 + W / 2 + NCAP / 8 + 8 + W + NCAP);
-  auto kfn = aca_cluster_kernel<DIM, KIND, KC, CL>;
-  HM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  // one cluster per SM-group: CTAs = CL * min(jobs, SMs / CL * 2)
-  const long long clusters = std::min<long long>(J.njobs, std::max(1, 2 * sms / CL));
-  kfn<<<static_cast<unsigned>(clusters * CL), 256, smem, s>>>(J, E);
-  HM_LAUNCH_CHECK();
-}
-
-template <int DIM, int KIND, int KC>
-void launch_big(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int max_rows, int sms, cudaStream_t s) {
-  if (J.njobs <= 0) return;
-  const int mask_words = (max_rows + 31) / 32;
-  const size_t smem = ((mask_words + 1) / 2 + kKmax + 40) * sizeof(double);
-  auto kfn = aca_big_kernel<DIM, KIND, KC>;
-  HM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  int occ = 0;
-  HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kBigThreads, smem));
-  const long long ctas = std::min<long long>(J.njobs, static_cast<long long>(std::max(occ, 1)) * sms);
-  // per-CTA window of kBigW columns (L2-resident)
-  DevBuf<double> scratch;
-  const long long gstride = max_rows + 1;
-  scratch.alloc(static_cast<size_t>(gstride) * kBigW * ctas, s);
-  kfn<<<static_cast<unsigned>(std::max(ctas, 1ll)), kBigThreads, smem, s>>>(J, E, scratch.get(), gstride, mask_words);
-  HM_LAUNCH_CHECK();
-}
-
-// ACA size classes: team kernels for max(m, n) <= 64 * NW (NW = 1, 2, 4, 8), the
-// CTA kernel for larger blocks, for k > 32 and for the epsilon criterion.
-constexpr int kAcaClasses = 9;
-constexpr int kAcaCl4 = 5;                // aca_cluster_kernel, 4 CTAs (<= 2048 rows)
-constexpr int kAcaCl8 = 6;                // aca_cluster_kernel, 8 CTAs (<= 4096 rows)
-constexpr int kAcaBig = 7;                // aca_big_kernel
-constexpr int kAcaCta = kAcaClasses - 1;  // the general CTA kernel (epsilon criterion, k > 32)
-__host__ __device__ inline int aca_class(int m, int n, long long kmax, bool has_eps, bool clusters = true) {
-  if (has_eps || kmax > 32) return kAcaCta;
-  const int c = m > n ? m : n;
-  if (c <= 1024) return c <= 64 ? 0 : c <= 128 ? 1 : c <= 256 ? 2 : c <= 512 ? 3 : 4;
-  if (clusters && c <= 2048) return kAcaCl4;
-  if (clusters && c <= 4096) return kAcaCl8;
-  return kAcaBig;
-}
 
 __global__ void class_key_kernel(const int* __restrict__ m, const int* __restrict__ nn, long long begin, long long cnt,
                                  int kmax, int has_eps, int clusters, unsigned long long* __restrict__ keys,
@@ -1512,213 +36,135 @@ __global__ void size_key_kernel(const int* __restrict__ m, const int* __restrict
 
 }  // namespace
 
-// Factorises aca leaves [leaf_begin, leaf_end) into h.U / h.V at offsets
-// h.u_off[b] - h.u_off[leaf_begin] (so a chunk workspace can be reused).
-void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStream_t s) {
-  const long long cnt = leaf_end - leaf_begin;
+// epsilon criterion (aca.cpp:497-538) is live only for eta <= 1: the bound is
+// eps (1 - eta) / (1 + eps) * ||A_r||_F, negative for eta > 1, while ||u_r|| ||v_r|| >= 0
+// (u_r[p] = 1), so the stop test can never fire -- such blocks run on the
+// fast size-class kernels with identical results.
+static bool eps_live(const HMatrix& h) {
+  if (!h.cfg.has_epsilon) return false;
+  const double f = h.cfg.epsilon * (1.0 - h.cfg.eta) / (1.0 + h.cfg.epsilon);
+  return !(f < 0.0);
+}
+
+void reset_aca_rejections(HMatrix& h, cudaStream_t s) {
+  if (h.aca_rej.size() < 2) h.aca_rej.alloc(2, s);
+  h.aca_rej.zero(s);
+}
+
+// Schedule of aca leaves [c.c0, c.c1): the long-leaves-first order of the V^T x fold and
+// the per-class job lists (largest n first within a class), both sorted once here.
+void plan_aca_chunk(HMatrix& h, AcaChunk& c, cudaStream_t s) {
+  const long long cnt = c.c1 - c.c0;
+  for (int q = 0; q < kAcaClasses; ++q) c.ccount[q] = 0;
+  c.max_rows_big = 0;
   if (cnt <= 0) return;
   if (h.cfg.k > kKmax) raise(kEinval, "k > 64 is not supported by the device ACA");
-  PhaseTrace tr, tra;
-  tr.mark("start", s);
-  // largest-first schedule
+  if (h.sched_jobs.size() < static_cast<size_t>(c.sched_off + cnt))
+    raise(kElogic, "plan_aca_chunk: schedule buffer too small");
+  const bool eps = eps_live(h);
+  const bool clus = std::getenv("HM_NO_CLUSTER") == nullptr;
+  for (long long b = c.c0; b < c.c1; ++b) {
+    const int q = aca_class(h.aca.h_m[b], h.aca.h_n[b], h.cfg.k, eps, clus);
+    ++c.ccount[q];
+    if (q == kAcaBig) c.max_rows_big = std::max(c.max_rows_big, h.aca.h_m[b]);
+  }
   DevBuf<unsigned long long> keys;
   keys.alloc(cnt, s);
-  h.aca_order.alloc(cnt, s);
-  size_key_kernel<<<grid_for(cnt, 256, 1 << 16), 256, 0, s>>>(h.aca.m.get(), h.aca.n.get(), h.aca.cl.get(), leaf_begin,
-                                                               cnt,
-                                                               keys.get(), reinterpret_cast<unsigned*>(h.aca_order.get()));
+  unsigned* order = reinterpret_cast<unsigned*>(h.sched_order.get() + c.sched_off);
+  unsigned* jobs = reinterpret_cast<unsigned*>(h.sched_jobs.get() + c.sched_off);
+  size_key_kernel<<<grid_for(cnt, 256, 1 << 16), 256, 0, s>>>(h.aca.m.get(), h.aca.n.get(), h.aca.cl.get(), c.c0, cnt,
+                                                               keys.get(), order);
   HM_LAUNCH_CHECK();
-  radix_sort_pairs(keys.get(), reinterpret_cast<unsigned*>(h.aca_order.get()), cnt, s);
-  h.aca_long_jobs = 0;
-  for (long long b = leaf_begin; b < leaf_end; ++b) h.aca_long_jobs += h.aca.h_n[b] >= 2048 ? 1 : 0;
-  h.counter.alloc(1, s);
-  h.counter.zero(s);
-  DevBuf<unsigned long long> rej;
-  rej.alloc(1, s);
-  rej.zero(s);
-  long long ub = 0, vb = 0;
-  HM_CUDA(cudaMemcpyAsync(&ub, h.u_off.get() + leaf_begin, sizeof(long long), cudaMemcpyDeviceToHost, s));
-  HM_CUDA(cudaMemcpyAsync(&vb, h.v_off.get() + leaf_begin, sizeof(long long), cudaMemcpyDeviceToHost, s));
-  HM_CUDA(cudaStreamSynchronize(s));
+  radix_sort_pairs(keys.get(), order, cnt, s);
+  class_key_kernel<<<grid_for(cnt, 256, 1 << 16), 256, 0, s>>>(h.aca.m.get(), h.aca.n.get(), c.c0, cnt,
+                                                                static_cast<int>(h.cfg.k), eps ? 1 : 0, clus ? 1 : 0,
+                                                                keys.get(), jobs);
+  HM_LAUNCH_CHECK();
+  radix_sort_pairs(keys.get(), jobs, cnt, s);
+}
+
+// Factorises the planned chunk c into h.U / h.V at offsets h.u_off[b] - c.ub (so a chunk
+// workspace can be reused).  Stream-ordered only: no host synchronisation.
+void compute_aca(HMatrix& h, const AcaChunk& c, cudaStream_t s) {
+  const long long cnt = c.c1 - c.c0;
+  if (cnt <= 0) return;
+  PhaseTrace tr;
+  tr.mark("start", s);
+  if (h.aca_counters.size() < static_cast<size_t>(kAcaClasses)) h.aca_counters.alloc(kAcaClasses, s);
+  h.aca_counters.zero(s);
+  if (h.aca_rej.size() < 2) reset_aca_rejections(h, s);
   AcaJob J{};
   J.rl = h.aca.rl.get();
   J.m = h.aca.m.get();
   J.cl = h.aca.cl.get();
   J.nn = h.aca.n.get();
-  J.order = h.aca_order.get();
+  J.order = nullptr;
   J.njobs = cnt;
   J.u_off = h.u_off.get();
   J.v_off = h.v_off.get();
-  J.u_base = ub;
-  J.v_base = vb;
+  J.u_base = c.ub;
+  J.v_base = c.vb;
   J.U = h.U.get();
   J.V = h.V.get();
   J.k_eff = h.k_eff.get();
   J.row_piv = h.row_piv.get();
   J.col_piv = h.col_piv.get();
   J.kmax = static_cast<int>(h.cfg.k);
-  J.has_eps = h.cfg.has_epsilon ? 1 : 0;
+  J.has_eps = eps_live(h) ? 1 : 0;
   J.eps_factor = h.cfg.epsilon * (1.0 - h.cfg.eta) / (1.0 + h.cfg.epsilon);
-  J.counter = h.counter.get();
-  J.rejections = rej.get();
+  J.rejections = h.aca_rej.get();
   J.evals = nullptr;
   J.tile_shift = h.u_tile_shift;
-  // size classes (team kernels for small blocks, the CTA kernel for the rest)
-  const bool eps = h.cfg.has_epsilon;
-  const bool clus = std::getenv("HM_NO_CLUSTER") == nullptr;
-  long long ccount[kAcaClasses] = {};
-  for (long long b = leaf_begin; b < leaf_end; ++b)
-    ++ccount[aca_class(h.aca.h_m[b], h.aca.h_n[b], h.cfg.k, eps, clus)];
-  DevBuf<int> jobs;
-  jobs.alloc(cnt, s);
-  class_key_kernel<<<grid_for(cnt, 256, 1 << 16), 256, 0, s>>>(h.aca.m.get(), h.aca.n.get(), leaf_begin, cnt,
-                                                                static_cast<int>(h.cfg.k), eps ? 1 : 0, clus ? 1 : 0,
-                                                                keys.get(),
-                                                                reinterpret_cast<unsigned*>(jobs.get()));
-  HM_LAUNCH_CHECK();
-  radix_sort_pairs(keys.get(), reinterpret_cast<unsigned*>(jobs.get()), cnt, s);
-  tr.mark("schedules (2 sorts)", s);
-  DevBuf<int> counters;
-  counters.alloc(kAcaClasses, s);
-  counters.zero(s);
+  const int* jobs = h.sched_jobs.get() + c.sched_off;
+  const long long* ccount = c.ccount;
   int sms = 0;
   HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h.device));
   long long first[kAcaClasses + 1];
   first[0] = 0;
-  for (int c = 0; c < kAcaClasses; ++c) first[c + 1] = first[c] + ccount[c];
+  for (int q = 0; q < kAcaClasses; ++q) first[q + 1] = first[q] + ccount[q];
   DevBuf<unsigned long long> evals;
   if (tr.on) {
     evals.alloc(3 * kAcaClasses, s);
     evals.zero(s);
   }
-  auto sub = [&](int c) {
+  auto sub = [&](int q) {
     AcaJob Jc = J;
-    Jc.evals = tr.on ? evals.get() + 3 * c : nullptr;
-    Jc.order = jobs.get() + first[c];
-    Jc.njobs = ccount[c];
-    Jc.counter = counters.get() + c;
+    Jc.evals = tr.on ? evals.get() + 3 * q : nullptr;
+    Jc.order = jobs + first[q];
+    Jc.njobs = ccount[q];
+    Jc.counter = h.aca_counters.get() + q;
     return Jc;
   };
-  // large blocks on the auxiliary stream, concurrently with the team kernels
-  // the CTA kernel (largest blocks first, long per-block latency) runs first, on the
-  // same stream: sharing SMs with the window kernels starves their 1-CTA/SM launches
-  const bool cta_aux = std::getenv("HM_ACA_AUX") != nullptr;
-  cudaStream_t sc = cta_aux ? h.aux : s;
-  if (ccount[kAcaCta] > 0) {
-    if (cta_aux) {
-      HM_CUDA(cudaEventRecord(h.ev_fork, s));
-      HM_CUDA(cudaStreamWaitEvent(h.aux, h.ev_fork, 0));
-    }
-    const AcaJob Jb = sub(kAcaCta);
-    tra.mark("start", sc);
-    switch (h.d) {
-      case 1: launch_kernel_aca<1>(Jb, h, sc); break;
-      case 2: launch_kernel_aca<2>(Jb, h, sc); break;
-      case 3: launch_kernel_aca<3>(Jb, h, sc); break;
-      case 4: launch_kernel_aca<4>(Jb, h, sc); break;
-      default: launch_kernel_aca<0>(Jb, h, sc); break;
-    }
-    tra.mark("cta kernel (>1024)", sc);
-    if (!cta_aux) tr.mark("cta kernel (>1024)", s);
-  }
-  auto teams_kind = [&](auto dimc, auto kindc) {
-    constexpr int DIM = decltype(dimc)::value;
-    constexpr int KIND = decltype(kindc)::value;
-    KernelEntry<DIM, KIND> E{h.coords.get(), h.n, h.d, h.kp};
-    if (h.cfg.k <= 16) {
-      launch_cluster<DIM, KIND, 16, 4>(sub(kAcaCl4), E, sms, s);
-      launch_cluster<DIM, KIND, 16, 8>(sub(kAcaCl8), E, sms, s);
-    } else {
-      launch_cluster<DIM, KIND, 32, 4>(sub(kAcaCl4), E, sms, s);
-      launch_cluster<DIM, KIND, 32, 8>(sub(kAcaCl8), E, sms, s);
-    }
-    tr.mark("clusters (<=4096)", s);
-    if (ccount[kAcaBig] > 0) {
-      int max_rows = 0;
-      for (long long b = leaf_begin; b < leaf_end; ++b)
-        if (aca_class(h.aca.h_m[b], h.aca.h_n[b], h.cfg.k, eps, clus) == kAcaBig)
-          max_rows = std::max(max_rows, h.aca.h_m[b]);
-      if (tr.on && std::getenv("HM_TRACE_BIG")) {  // per-size sub-launches (jobs are sorted by n descending)
-        const int edges[] = {1 << 30, 16384, 8192, 4096, 2048, 0};
-        AcaJob Jb = sub(kAcaBig);
-        long long off = 0;
-        for (int e = 0; e < 5; ++e) {
-          long long c = 0;
-          for (long long b = leaf_begin; b < leaf_end; ++b)
-            if (aca_class(h.aca.h_m[b], h.aca.h_n[b], h.cfg.k, eps, clus) == kAcaBig && h.aca.h_n[b] < edges[e] &&
-                h.aca.h_n[b] >= edges[e + 1])
-              ++c;
-          AcaJob Je = Jb;
-          Je.order = Jb.order + off;
-          Je.njobs = c;
-          HM_CUDA(cudaMemsetAsync(Je.counter, 0, sizeof(int), s));
-          if (c) launch_big<DIM, KIND, 16>(Je, E, max_rows, sms, s);
-          static char names[5][48];
-          std::snprintf(names[e], sizeof(names[e]), "big n in [%d,%d): %lld", edges[e + 1], edges[e], c);
-          tr.mark(names[e], s);
-          off += c;
-        }
-      } else {
-        if (h.cfg.k <= 16) launch_big<DIM, KIND, 16>(sub(kAcaBig), E, max_rows, sms, s);
-        else launch_big<DIM, KIND, 32>(sub(kAcaBig), E, max_rows, sms, s);
-        tr.mark("big (>1024)", s);
-      }
-    }
-    if (h.cfg.k <= 16) {
-      launch_win<DIM, KIND, 16, 16, 8, true>(sub(4), E, sms, s);
-      tr.mark("win NW=16 (<=1024)", s);
-      launch_win<DIM, KIND, 8, 16, 8, true, 2>(sub(3), E, sms, s);
-      tr.mark("NW=8 (<=512)", s);
-      launch_win<DIM, KIND, 4, 16, 16, true, 3>(sub(2), E, sms, s);
-      tr.mark("NW=4 (<=256)", s);
-      // the small blocks are latency-bound: registers capped for 12 warps per SM (ncu: at
-      // 208 registers / 8 warps the <= 64 class issues at IPC ~1.5, at 128 it spends 20% of
-      // its instructions rematerialising addresses; 3 CTAs per SM is the measured optimum)
-      launch_win<DIM, KIND, 2, 16, 16, true, 3>(sub(1), E, sms, s);
-      tr.mark("NW=2 (<=128)", s);
-      launch_win<DIM, KIND, 1, 16, 8, true, 3>(sub(0), E, sms, s);
-      tr.mark("NW=1 (<=64)", s);
-    } else {
-      launch_win<DIM, KIND, 16, 32, 16, false>(sub(4), E, sms, s);
-      launch_win<DIM, KIND, 8, 32, 32, false>(sub(3), E, sms, s);
-      launch_win<DIM, KIND, 4, 32, 32, false>(sub(2), E, sms, s);
-      launch_win<DIM, KIND, 2, 32, 16, true>(sub(1), E, sms, s);
-      launch_win<DIM, KIND, 1, 32, 16, true>(sub(0), E, sms, s);
-    }
-  };
-  auto teams_for = [&](auto dimc) {
-    if (h.kp.kind == kGaussian) teams_kind(dimc, std::integral_constant<int, 0>{});
-    else teams_kind(dimc, std::integral_constant<int, 1>{});
-  };
+  AcaClassLaunch L;
+  for (int q = 0; q < kAcaClasses; ++q) L.J[q] = sub(q);
+  L.sms = sms;
+  L.max_rows_big = c.max_rows_big;
+  L.kind = h.kp.kind;
+  L.kp = h.kp;
+  L.coords = h.coords.get();
+  L.n = h.n;
+  L.d = h.d;
+  L.device = h.device;
+  L.big_scratch = &h.aca_big_scratch;
+  L.tr = &tr;
   switch (h.d) {
-    case 1: teams_for(std::integral_constant<int, 1>{}); break;
-    case 2: teams_for(std::integral_constant<int, 2>{}); break;
-    case 3: teams_for(std::integral_constant<int, 3>{}); break;
-    case 4: teams_for(std::integral_constant<int, 4>{}); break;
-    default: teams_for(std::integral_constant<int, 0>{}); break;
+    case 1: aca_classes_d1(L, s); break;
+    case 2: aca_classes_d2(L, s); break;
+    case 3: aca_classes_d3(L, s); break;
+    case 4: aca_classes_d4(L, s); break;
+    default: aca_classes_d0(L, s); break;
   }
-  if (ccount[kAcaCta] > 0 && cta_aux) {
-    HM_CUDA(cudaEventRecord(h.ev_join, h.aux));
-    HM_CUDA(cudaStreamWaitEvent(s, h.ev_join, 0));
-  }
-  tr.mark("join", s);
-  if (tr.on)
+  if (tr.on) {
     std::fprintf(stderr, "[hm_trace] aca classes: %lld %lld %lld %lld %lld | cl4 %lld cl8 %lld big %lld cta %lld\n",
                  ccount[0], ccount[1], ccount[2], ccount[3], ccount[4], ccount[5], ccount[6], ccount[7], ccount[8]);
-  tr.dump();
-  tra.dump();
-  if (tr.on) {
+    tr.dump();
     unsigned long long ev[3 * kAcaClasses];
     HM_CUDA(cudaMemcpyAsync(ev, evals.get(), sizeof(ev), cudaMemcpyDeviceToHost, s));
     HM_CUDA(cudaStreamSynchronize(s));
-    for (int c = 0; c < kAcaClasses; ++c)
-      std::fprintf(stderr, "[hm_trace] class %d: blocks %llu col-entries %.4g row-entries %.4g\n", c, ev[3 * c + 2],
-                   static_cast<double>(ev[3 * c]), static_cast<double>(ev[3 * c + 1]));
+    for (int q = 0; q < kAcaClasses; ++q)
+      std::fprintf(stderr, "[hm_trace] class %d: blocks %llu col-entries %.4g row-entries %.4g\n", q, ev[3 * q + 2],
+                   static_cast<double>(ev[3 * q]), static_cast<double>(ev[3 * q + 1]));
   }
-  unsigned long long hrej = 0;
-  HM_CUDA(cudaMemcpyAsync(&hrej, rej.get(), sizeof(hrej), cudaMemcpyDeviceToHost, s));
-  HM_CUDA(cudaStreamSynchronize(s));
-  h.aca_rejections += static_cast<long long>(hrej);
 }
 
 // Explicit-matrix seam (aca.cpp:567-578): host blocks in, host factors out in the

@@ -1,0 +1,73 @@
+// aca_dim.cu -- the ACA size-class kernels instantiated for ONE point dimension
+// (compiled once per HM_ACA_DIM in {0 (generic d > 4), 1, 2, 3, 4}, see Makefile), so the
+// heavy template instantiations build in parallel.  Launch order per chunk: the general
+// CTA kernel (epsilon criterion / k > 32), the cluster kernels, the big-block kernel,
+// then the window kernels from the largest class down (largest-first within a class).
+#include "aca_impl.cuh"
+
+#ifndef HM_ACA_DIM
+#error "compile with -DHM_ACA_DIM=<0..4>"
+#endif
+#define HM_CAT2(a, b) a##b
+#define HM_CAT(a, b) HM_CAT2(a, b)
+
+namespace hmb {
+namespace aca_detail {
+
+template <int DIM, int KIND>
+static void classes_kind(const AcaClassLaunch& L, cudaStream_t s) {
+  KernelEntry<DIM, KIND> E{L.coords, L.n, L.d, L.kp};
+  PhaseTrace& tr = *L.tr;
+  const int kmax = L.J[0].kmax;
+  const int sms = L.sms;
+  if (kmax <= 16) {
+    launch_cluster<DIM, KIND, 16, 4>(L.J[kAcaCl4], E, sms, s);
+    launch_cluster<DIM, KIND, 16, 8>(L.J[kAcaCl8], E, sms, s);
+  } else {
+    launch_cluster<DIM, KIND, 32, 4>(L.J[kAcaCl4], E, sms, s);
+    launch_cluster<DIM, KIND, 32, 8>(L.J[kAcaCl8], E, sms, s);
+  }
+  tr.mark("clusters (<=4096)", s);
+  if (L.J[kAcaBig].njobs > 0) {
+    if (kmax <= 16) launch_big<DIM, KIND, 16>(L.J[kAcaBig], E, L.max_rows_big, sms, *L.big_scratch, s);
+    else launch_big<DIM, KIND, 32>(L.J[kAcaBig], E, L.max_rows_big, sms, *L.big_scratch, s);
+    tr.mark("big (>4096)", s);
+  }
+  if (kmax <= 16) {
+    launch_win<DIM, KIND, 16, 16, 8, true>(L.J[4], E, sms, s);
+    tr.mark("win NW=16 (<=1024)", s);
+    launch_win<DIM, KIND, 8, 16, 8, true, 2>(L.J[3], E, sms, s);
+    tr.mark("NW=8 (<=512)", s);
+    launch_win<DIM, KIND, 4, 16, 16, true, 3>(L.J[2], E, sms, s);
+    tr.mark("NW=4 (<=256)", s);
+    // the small blocks are latency-bound: registers capped for 12 warps per SM (ncu: at
+    // 208 registers / 8 warps the <= 64 class issues at IPC ~1.5, at 128 it spends 20% of
+    // its instructions rematerialising addresses; 3 CTAs per SM is the measured optimum)
+    launch_win<DIM, KIND, 2, 16, 16, true, 3>(L.J[1], E, sms, s);
+    tr.mark("NW=2 (<=128)", s);
+    launch_win<DIM, KIND, 1, 16, 8, true, 3>(L.J[0], E, sms, s);
+    tr.mark("NW=1 (<=64)", s);
+  } else {
+    launch_win<DIM, KIND, 16, 32, 16, false>(L.J[4], E, sms, s);
+    launch_win<DIM, KIND, 8, 32, 32, false>(L.J[3], E, sms, s);
+    launch_win<DIM, KIND, 4, 32, 32, false>(L.J[2], E, sms, s);
+    launch_win<DIM, KIND, 2, 32, 16, true>(L.J[1], E, sms, s);
+    launch_win<DIM, KIND, 1, 32, 16, true>(L.J[0], E, sms, s);
+  }
+}
+
+void HM_CAT(aca_classes_d, HM_ACA_DIM)(const AcaClassLaunch& L, cudaStream_t s) {
+  constexpr int DIM = HM_ACA_DIM;
+  if (L.J[kAcaCta].njobs > 0) {
+    // the CTA kernel runs first on the same stream: sharing SMs with the window kernels
+    // starves their 1-CTA/SM launches
+    KernelEntry<DIM> E{L.coords, L.n, L.d, L.kp};
+    launch_kernel_aca<DIM>(L.J[kAcaCta], E, L.sms, s);
+    L.tr->mark("cta kernel", s);
+  }
+  if (L.kind == kGaussian) classes_kind<DIM, 0>(L, s);
+  else classes_kind<DIM, 1>(L, s);
+}
+
+}  // namespace aca_detail
+}  // namespace hmb

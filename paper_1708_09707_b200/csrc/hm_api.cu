@@ -28,6 +28,19 @@ struct hm_handle {
   std::mutex mu;
   ncclComm_t comm = nullptr;
   std::vector<long long> rank_bounds;  // Morton row slice [b[r], b[r+1]) of every rank
+  bool equal_slices = false;           // all slices the same size: one ncclAllGather
+  // pinned staging of hm_mvp's host vectors (H2D / D2H at full PCIe rate)
+  double* pin_x = nullptr;
+  double* pin_z = nullptr;
+  // CG scalars read back once per iteration
+  double* pin_scal = nullptr;
+  size_t pin_scal_n = 0;
+  ~hm_handle() {
+    if (comm) hmb::NcclApi::get().CommDestroy(comm);
+    if (pin_x) cudaFreeHost(pin_x);
+    if (pin_z) cudaFreeHost(pin_z);
+    if (pin_scal) cudaFreeHost(pin_scal);
+  }
 };
 
 namespace {
@@ -137,20 +150,36 @@ void setup_common(hm_handle* H, const double* coords_dev, long long n, int d) {
 
 hm_handle* new_handle(const hm_config* cfg, long long n, int d, int kernel, double beta) {
   require_device();
-  auto H = std::make_unique<hm_handle>();
-  H->h.cfg = to_config(cfg);
-  H->h.device = cfg ? cfg->device : 0;
-  HM_CUDA(cudaSetDevice(H->h.device));
-  HM_CUDA(cudaStreamCreateWithFlags(&H->h.stream, cudaStreamNonBlocking));
-  HM_CUDA(cudaStreamCreateWithFlags(&H->h.aux, cudaStreamNonBlocking));
-  HM_CUDA(cudaEventCreateWithFlags(&H->h.ev_fork, cudaEventDisableTiming));
-  HM_CUDA(cudaEventCreateWithFlags(&H->h.ev_join, cudaEventDisableTiming));
-  H->h.kp = make_kernel(kernel, beta, d);
-  H->h.n = n;
-  H->h.d = d;
+  // validate everything before any CUDA object exists
+  const Config c = to_config(cfg);
   if (n < 1) raise(kEinval, "build_block_cluster_tree: empty point set");
   if (d < 1 || d > 20) raise(kEinval, "dimension must be in [1, 20]");
+  const KernelParams kp = make_kernel(kernel, beta, d);
+  auto H = std::make_unique<hm_handle>();
+  H->h.cfg = c;
+  H->h.kp = kp;
+  H->h.n = n;
+  H->h.d = d;
+  H->h.create(cfg ? cfg->device : 0);  // streams + events, released by ~HandleStreams
   return H.release();
+}
+
+// Runs f(stream) on the handle's stream, ordered after the work already queued on
+// `caller` and with `caller` ordered after it (event fork/join: capture-safe, so the
+// call can be recorded into a CUDA graph on the caller's stream).  All handle work and
+// all workspace allocations stay on h.stream, so products issued from different
+// caller streams are serialised on the device, not just on the host mutex.
+template <class F>
+void on_handle_stream(HMatrix& h, cudaStream_t caller, F&& f) {
+  if (caller == nullptr || caller == h.stream) {
+    f(h.stream);
+    return;
+  }
+  HM_CUDA(cudaEventRecord(h.ev_join, caller));
+  HM_CUDA(cudaStreamWaitEvent(h.stream, h.ev_join, 0));
+  f(h.stream);
+  HM_CUDA(cudaEventRecord(h.ev_last, h.stream));
+  HM_CUDA(cudaStreamWaitEvent(caller, h.ev_last, 0));
 }
 
 // ---------------------------------------------------------------- small kernels
@@ -207,61 +236,109 @@ __global__ void scatter_kernel(const double* __restrict__ zm, const long long* _
     z[perm[i]] = zm[i];
 }
 
-// fixed-order deterministic dot: per-block tree partials, then one block folds them
-__global__ void dot_partial_kernel(const double* a, const double* b, long long n, double* part) {
+// ---------------------------------------------------------------- CG on the device
+// R columns (column r at base + r*n).  Scalars stay on the device; the host reads them
+// once per iteration (the stopping rule).  Dots are fixed-order (per-block tree
+// partials folded in block order), so every run gives the same bits.
+constexpr int kDotBlocks = 296;  // 2 x 148 SMs per column
+
+__global__ void dots_partial_kernel(const double* a, const double* b, long long n, double* part) {
   __shared__ double sm[256];
+  const long long off = static_cast<long long>(blockIdx.y) * n;
   double acc = 0.0;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
-    acc = hadd(acc, hmul(a[i], b[i]));
+    acc = hadd(acc, hmul(a[off + i], b[off + i]));
   sm[threadIdx.x] = acc;
   __syncthreads();
   for (int s = 128; s; s >>= 1) {
     if (threadIdx.x < s) sm[threadIdx.x] = hadd(sm[threadIdx.x], sm[threadIdx.x + s]);
     __syncthreads();
   }
-  if (threadIdx.x == 0) part[blockIdx.x] = sm[0];
+  if (threadIdx.x == 0) part[static_cast<long long>(blockIdx.y) * gridDim.x + blockIdx.x] = sm[0];
 }
-__global__ void dot_final_kernel(const double* part, int nb, double* out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double acc = 0.0;
-    for (int i = 0; i < nb; ++i) acc = hadd(acc, part[i]);
-    *out = acc;
+// out[r] = fold of column r's partials; op 0: store, 1: alpha = rs / out (active columns),
+// 2: beta = out / rs, rs = out
+__global__ void dots_final_kernel(const double* part, int nb, int R, double* out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  double acc = 0.0;
+  for (int i = 0; i < nb; ++i) acc = hadd(acc, part[static_cast<long long>(r) * nb + i]);
+  out[r] = acc;
+}
+__global__ void cg_alpha_kernel(const double* rs, const double* pap, const int* active, double* alpha, int R) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < R) alpha[r] = active[r] ? __ddiv_rn(rs[r], pap[r]) : 0.0;
+}
+__global__ void cg_beta_kernel(double* rs, const double* rs_next, const int* active, double* beta, int R) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < R && active[r]) {
+    beta[r] = __ddiv_rn(rs_next[r], rs[r]);
+    rs[r] = rs_next[r];
   }
 }
-
-// CG vector updates (solver.cpp:27-31, 46-49, 59-61)
+// CG vector updates (solver.cpp:27-31, 46-49, 59-61), column r = blockIdx.y
 __global__ void axpy_sigma_kernel(double* ap, const double* p, double sigma2, long long n) {
+  const long long off = static_cast<long long>(blockIdx.y) * n;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
-    ap[i] = hadd(ap[i], hmul(sigma2, p[i]));
+    ap[off + i] = hadd(ap[off + i], hmul(sigma2, p[off + i]));
 }
-__global__ void cg_update_kernel(double* x, double* r, const double* p, const double* ap, const double* alpha_p,
-                                 long long n) {
-  const double alpha = *alpha_p;
+__global__ void cg_update_kernel(double* x, double* r, const double* p, const double* ap, const double* alpha,
+                                 const int* active, long long n) {
+  if (!active[blockIdx.y]) return;
+  const double al = alpha[blockIdx.y];
+  const long long off = static_cast<long long>(blockIdx.y) * n;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    x[i] = hadd(x[i], hmul(alpha, p[i]));
-    r[i] = hsub(r[i], hmul(alpha, ap[i]));
+    x[off + i] = hadd(x[off + i], hmul(al, p[off + i]));
+    r[off + i] = hsub(r[off + i], hmul(al, ap[off + i]));
   }
 }
-__global__ void cg_dir_kernel(double* p, const double* r, double beta, long long n) {
+__global__ void cg_dir_kernel(double* p, const double* r, const double* beta, const int* active, long long n) {
+  if (!active[blockIdx.y]) return;
+  const double be = beta[blockIdx.y];
+  const long long off = static_cast<long long>(blockIdx.y) * n;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
-    p[i] = hadd(r[i], hmul(beta, p[i]));
+    p[off + i] = hadd(r[off + i], hmul(be, p[off + i]));
+}
+__global__ void sub_kernel(double* d, const double* b, long long total) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    d[i] = hsub(b[i], d[i]);
 }
 
-constexpr int kDotBlocks = 1184;  // 8 x 148 SMs
-
-double device_dot(const double* a, const double* b, long long n, DevBuf<double>& part, cudaStream_t s) {
-  if (part.size() < kDotBlocks + 1) part.alloc(kDotBlocks + 1, s);
-  dot_partial_kernel<<<kDotBlocks, 256, 0, s>>>(a, b, n, part.get());
-  dot_final_kernel<<<1, 32, 0, s>>>(part.get(), kDotBlocks, part.get() + kDotBlocks);
+// out[r] = a_r . b_r for R columns (device result)
+void device_dots(const double* a, const double* b, long long n, int R, DevBuf<double>& part, double* out,
+                 cudaStream_t s) {
+  if (part.size() < static_cast<size_t>(kDotBlocks) * R) part.alloc(static_cast<size_t>(kDotBlocks) * R, s);
+  dots_partial_kernel<<<dim3(kDotBlocks, R), 256, 0, s>>>(a, b, n, part.get());
+  dots_final_kernel<<<(R + 31) / 32, 32, 0, s>>>(part.get(), kDotBlocks, R, out);
   HM_LAUNCH_CHECK();
-  double out = 0.0;
-  HM_CUDA(cudaMemcpyAsync(&out, part.get() + kDotBlocks, sizeof(double), cudaMemcpyDeviceToHost, s));
-  HM_CUDA(cudaStreamSynchronize(s));
-  return out;
+}
+
+// y allgather: rank r's Morton rows [b[r], b[r+1]) of y are gathered in
+// place on every rank.  Equal slices (power-of-two N, the bench configurations): one
+// in-place ncclAllGather; otherwise grouped in-place broadcasts (ceil-split slices).
+void allgather_y(hm_handle* H, double* y, cudaStream_t s) {
+  HMatrix& h = H->h;
+  if (!H->comm) raise(kEnccl, "world > 1 but no NCCL communicator attached (hm_attach_nccl)");
+  const std::vector<long long>& bounds = H->rank_bounds;
+  const NcclApi& nc = NcclApi::get();
+  if (H->equal_slices) {
+    const size_t cnt = static_cast<size_t>(bounds[1] - bounds[0]);
+    if (nc.AllGather(y + bounds[h.cfg.rank], y, cnt, ncclDouble, H->comm, s) != ncclSuccess)
+      raise(kEnccl, "ncclAllGather of the y slices failed");
+    return;
+  }
+  if (nc.GroupStart() != ncclSuccess) raise(kEnccl, "ncclGroupStart");
+  for (int r = 0; r < h.cfg.world; ++r) {
+    double* p = y + bounds[r];
+    if (nc.Broadcast(p, p, static_cast<size_t>(bounds[r + 1] - bounds[r]), ncclDouble, r, H->comm, s) != ncclSuccess)
+      raise(kEnccl, "ncclBroadcast of the y slice failed");
+  }
+  if (nc.GroupEnd() != ncclSuccess) raise(kEnccl, "ncclGroupEnd");
 }
 
 // z (original order, device) = H x, with the row-sliced allgather when world > 1
@@ -274,20 +351,8 @@ void product(hm_handle* H, const double* x_dev, double* z_dev, cudaStream_t s) {
   h.clk.stop(kKGather, s);
   mvp_morton(h, s);
   if (h.cfg.world > 1) {
-    if (!H->comm) raise(kEnccl, "world > 1 but no NCCL communicator attached (hm_attach_nccl)");
-    // y allgather: each rank's Morton row slice is broadcast in place;
-    // slices are contiguous and may differ in size by the ceil splits.
-    const std::vector<long long>& bounds = H->rank_bounds;
     h.clk.start(kKAllgather, s);
-    const NcclApi& nc = NcclApi::get();
-    if (nc.GroupStart() != ncclSuccess) raise(kEnccl, "ncclGroupStart");
-    for (int r = 0; r < h.cfg.world; ++r) {
-      double* p = h.zm.get() + bounds[r];
-      if (nc.Broadcast(p, p, static_cast<size_t>(bounds[r + 1] - bounds[r]), ncclDouble, r, H->comm, s) !=
-          ncclSuccess)
-        raise(kEnccl, "ncclBroadcast of the y slice failed");
-    }
-    if (nc.GroupEnd() != ncclSuccess) raise(kEnccl, "ncclGroupEnd");
+    allgather_y(H, h.zm.get(), s);
     h.clk.stop(kKAllgather, s);
   }
   h.clk.start(kKScatter, s);
@@ -303,20 +368,8 @@ void product_multi(hm_handle* H, const double* X_dev, double* Z_dev, int R, int 
   ensure_multi(h, R, s);
   gather_multi(h, X_dev, n, R, s);
   mvp_multi_morton(h, R, flags, s);
-  if (h.cfg.world > 1) {
-    if (!H->comm) raise(kEnccl, "world > 1 but no NCCL communicator attached (hm_attach_nccl)");
-    const std::vector<long long>& bounds = H->rank_bounds;
-    const NcclApi& nc = NcclApi::get();
-    if (nc.GroupStart() != ncclSuccess) raise(kEnccl, "ncclGroupStart");
-    for (int r = 0; r < R; ++r)
-      for (int g = 0; g < h.cfg.world; ++g) {
-        double* p = h.zmR.get() + static_cast<long long>(r) * n + bounds[g];
-        if (nc.Broadcast(p, p, static_cast<size_t>(bounds[g + 1] - bounds[g]), ncclDouble, g, H->comm, s) !=
-            ncclSuccess)
-          raise(kEnccl, "ncclBroadcast of a y slice failed");
-      }
-    if (nc.GroupEnd() != ncclSuccess) raise(kEnccl, "ncclGroupEnd");
-  }
+  if (h.cfg.world > 1)
+    for (int r = 0; r < R; ++r) allgather_y(H, h.zmR.get() + static_cast<long long>(r) * n, s);
   scatter_multi(h, Z_dev, n, R, s);
 }
 
@@ -359,57 +412,47 @@ int hm_device_count(void) {
 
 hm_status hm_setup(const double* coords, int64_t n, int32_t d, int32_t kernel, double beta, const hm_config* cfg,
                    hm_handle** out) {
+  if (!out) {
+    g_err = "hm_setup: null output handle";
+    return HM_EINVAL;
+  }
   *out = nullptr;
-  hm_handle* H = nullptr;
+  std::unique_ptr<hm_handle> H;
   const hm_status st = guarded([&] {
     if (!coords) raise(kEinval, "coords is null");
-    H = new_handle(cfg, n, d, kernel, beta);
+    H.reset(new_handle(cfg, n, d, kernel, beta));
     DevBuf<double> c;
     c.alloc(static_cast<size_t>(n) * d, H->h.stream);
     HM_CUDA(cudaMemcpyAsync(c.get(), coords, sizeof(double) * n * d, cudaMemcpyHostToDevice, H->h.stream));
-    setup_common(H, c.get(), n, d);
+    setup_common(H.get(), c.get(), n, d);
   });
-  if (st != HM_OK) {
-    delete H;
-    return st;
-  }
-  *out = H;
-  return HM_OK;
+  if (st == HM_OK) *out = H.release();
+  return st;
 }
 
 hm_status hm_setup_device(const double* coords_dev, int64_t n, int32_t d, int32_t kernel, double beta,
                           const hm_config* cfg, hm_handle** out) {
+  if (!out) {
+    g_err = "hm_setup_device: null output handle";
+    return HM_EINVAL;
+  }
   *out = nullptr;
-  hm_handle* H = nullptr;
+  std::unique_ptr<hm_handle> H;
   const hm_status st = guarded([&] {
     if (!coords_dev) raise(kEinval, "coords is null");
-    H = new_handle(cfg, n, d, kernel, beta);
-    setup_common(H, coords_dev, n, d);
+    H.reset(new_handle(cfg, n, d, kernel, beta));
+    setup_common(H.get(), coords_dev, n, d);
   });
-  if (st != HM_OK) {
-    delete H;
-    return st;
-  }
-  *out = H;
-  return HM_OK;
+  if (st == HM_OK) *out = H.release();
+  return st;
 }
 
 void hm_destroy(hm_handle* H) {
   if (!H) return;
-  cudaSetDevice(H->h.device);
-  if (H->comm) NcclApi::get().CommDestroy(H->comm);
-  cudaStream_t s = H->h.stream, aux = H->h.aux;
-  cudaEvent_t e0 = H->h.ev_fork, e1 = H->h.ev_join;
-  cudaStreamSynchronize(s);
-  if (aux) cudaStreamSynchronize(aux);
-  delete H;  // buffers are freed on the stream
-  if (s) {
-    cudaStreamSynchronize(s);
-    cudaStreamDestroy(s);
+  {
+    std::lock_guard<std::mutex> lock(H->mu);  // no call on this handle is in flight
   }
-  if (aux) cudaStreamDestroy(aux);
-  if (e0) cudaEventDestroy(e0);
-  if (e1) cudaEventDestroy(e1);
+  delete H;  // ~hm_handle: NCCL comm, pinned staging; ~HandleStreams syncs, then destroys streams
 }
 
 hm_status hm_mvp(hm_handle* H, const double* x, double* z, hm_timings* t) {
@@ -420,13 +463,33 @@ hm_status hm_mvp(hm_handle* H, const double* x, double* z, hm_timings* t) {
     HM_CUDA(cudaSetDevice(h.device));
     const auto t0 = Clock::now();
     cudaStream_t s = h.stream;
+    const size_t bytes = sizeof(double) * h.n;
     if (h.xin.size() < static_cast<size_t>(h.n)) h.xin.alloc(h.n, s);
     if (h.zout.size() < static_cast<size_t>(h.n)) h.zout.alloc(h.n, s);
-    HM_CUDA(cudaMemcpyAsync(h.xin.get(), x, sizeof(double) * h.n, cudaMemcpyHostToDevice, s));
-    product(H, h.xin.get(), h.zout.get(), s);
-    HM_CUDA(cudaMemcpyAsync(z, h.zout.get(), sizeof(double) * h.n, cudaMemcpyDeviceToHost, s));
+    // pinned staging: the copies run at full link rate (pageable copies are bounced
+    // through a driver buffer at a fraction of it)
+    if (!H->pin_x) HM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&H->pin_x), bytes));
+    if (!H->pin_z) HM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&H->pin_z), bytes));
+    std::memcpy(H->pin_x, x, bytes);
+    HM_CUDA(cudaMemcpyAsync(h.xin.get(), H->pin_x, bytes, cudaMemcpyHostToDevice, s));
+    h.phase_events = true;
+    try {
+      product(H, h.xin.get(), h.zout.get(), s);
+    } catch (...) {
+      h.phase_events = false;
+      throw;
+    }
+    h.phase_events = false;
+    HM_CUDA(cudaMemcpyAsync(H->pin_z, h.zout.get(), bytes, cudaMemcpyDeviceToHost, s));
     HM_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(z, H->pin_z, bytes);
     h.tm.mvp_ms = ms_since(t0);
+    // MvpTimings (hmatrix.cpp:117-121): dense (near-field) and ACA (far-field) phases
+    float dms = 0.f, ams = 0.f;
+    HM_CUDA(cudaEventElapsedTime(&dms, h.ev_ph[0], h.ev_ph[1]));
+    HM_CUDA(cudaEventElapsedTime(&ams, h.ev_ph[2], h.ev_ph[3]));
+    h.tm.mvp_dense_ms = dms;
+    h.tm.mvp_aca_ms = ams;
     if (t) hm_get_timings(H, t);
   });
 }
@@ -436,8 +499,7 @@ hm_status hm_mvp_device(hm_handle* H, const double* x_dev, double* z_dev, void* 
     if (!H || !x_dev || !z_dev) raise(kEinval, "mvp: null argument");
     std::lock_guard<std::mutex> lock(H->mu);
     HM_CUDA(cudaSetDevice(H->h.device));
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : H->h.stream;
-    product(H, x_dev, z_dev, s);
+    on_handle_stream(H->h, static_cast<cudaStream_t>(stream), [&](cudaStream_t s) { product(H, x_dev, z_dev, s); });
   });
 }
 
@@ -461,6 +523,7 @@ hm_status hm_mvp_local(hm_handle* H, const double* x, double* z_slice) {
 
 hm_status hm_nccl_unique_id(unsigned char id[128]) {
   return guarded([&] {
+    if (!id) raise(kEinval, "nccl_unique_id: null argument");
     ncclUniqueId u;
     if (NcclApi::get().GetUniqueId(&u) != ncclSuccess) raise(kEnccl, "ncclGetUniqueId failed");
     static_assert(sizeof(u) == 128, "ncclUniqueId size");
@@ -470,22 +533,32 @@ hm_status hm_nccl_unique_id(unsigned char id[128]) {
 
 hm_status hm_attach_nccl(hm_handle* H, const unsigned char id[128]) {
   return guarded([&] {
+    if (!H || !id) raise(kEinval, "attach_nccl: null argument");
+    std::lock_guard<std::mutex> lock(H->mu);
+    if (H->comm) raise(kEinval, "attach_nccl: a communicator is already attached to this handle");
     ncclUniqueId u;
     std::memcpy(&u, id, 128);
     HMatrix& h = H->h;
     HM_CUDA(cudaSetDevice(h.device));
-    if (NcclApi::get().CommInitRank(&H->comm, h.cfg.world, u, h.cfg.rank) != ncclSuccess)
+    ncclComm_t comm = nullptr;
+    if (NcclApi::get().CommInitRank(&comm, h.cfg.world, u, h.cfg.rank) != ncclSuccess)
       raise(kEnccl, "ncclCommInitRank failed");
+    H->comm = comm;
     int g = 0;
     while ((1 << g) < h.cfg.world) ++g;
     H->rank_bounds.assign(h.cfg.world + 1, h.n);
-    HM_CUDA(cudaMemcpy(H->rank_bounds.data(), h.slot_lo.get() + h.depth_base[g], sizeof(long long) * h.cfg.world,
-                       cudaMemcpyDeviceToHost));
+    HM_CUDA(cudaMemcpyAsync(H->rank_bounds.data(), h.slot_lo.get() + h.depth_base[g], sizeof(long long) * h.cfg.world,
+                            cudaMemcpyDeviceToHost, h.stream));
+    HM_CUDA(cudaStreamSynchronize(h.stream));
+    H->equal_slices = true;
+    for (int r = 0; r < h.cfg.world; ++r)
+      H->equal_slices &= (H->rank_bounds[r + 1] - H->rank_bounds[r]) == (H->rank_bounds[1] - H->rank_bounds[0]);
   });
 }
 
 hm_status hm_profile_begin(hm_handle* H) {
   return guarded([&] {
+    if (!H) raise(kEinval, "profile_begin: null handle");
     std::lock_guard<std::mutex> lock(H->mu);
     H->h.clk.on = true;
   });
@@ -493,6 +566,7 @@ hm_status hm_profile_begin(hm_handle* H) {
 
 hm_status hm_profile_end(hm_handle* H, double* ms, int64_t* counts) {
   return guarded([&] {
+    if (!H) raise(kEinval, "profile_end: null handle");
     std::lock_guard<std::mutex> lock(H->mu);
     KClock& c = H->h.clk;
     c.on = false;
@@ -515,71 +589,134 @@ hm_status hm_profile_end(hm_handle* H, double* ms, int64_t* counts) {
   });
 }
 
+namespace {
+
+// nrhs independent cg_solve runs (solver.cpp:19-73) in lock-step, device-resident: one
+// (multi-RHS) product per iteration, scalars on the device, ONE host read per iteration
+// for the stopping rule / non-finite check.  Each column keeps its own scalars and
+// stopping rule, so with flags = 0 (or R = 1) every column follows the single-RHS
+// iteration exactly.
+void cg_run(hm_handle* H, const double* B, long long R, double sigma2, double tol, long long max_iter, int flags,
+            bool multi, double* X, int64_t* iterations, double* rel_res) {
+  if (tol <= 0.0) raise(kEinval, "cg_solve: tol must be > 0");
+  if (max_iter < 1) raise(kEinval, "cg_solve: max_iter must be >= 1");
+  if (sigma2 < 0.0) raise(kEinval, "cg_solve: sigma2 must be >= 0");
+  HMatrix& h = H->h;
+  HM_CUDA(cudaSetDevice(h.device));
+  cudaStream_t s = h.stream;
+  const long long n = h.n;
+  const int Ri = static_cast<int>(R);
+  DevBuf<double> db, dx, dr, dp, dap, part, scal;
+  DevBuf<int> act;
+  db.alloc(n * R, s);
+  dx.alloc(n * R, s);
+  dr.alloc(n * R, s);
+  dp.alloc(n * R, s);
+  dap.alloc(n * R, s);
+  scal.alloc(6 * R, s);  // bn2 | rs | pap | rs_next | alpha | beta
+  act.alloc(R, s);
+  double* bn2 = scal.get();
+  double* rs = bn2 + R;
+  double* pap = rs + R;
+  double* rsn = pap + R;
+  double* alpha = rsn + R;
+  double* beta = alpha + R;
+  const size_t need = static_cast<size_t>(3 * R);
+  if (H->pin_scal_n < need) {
+    if (H->pin_scal) cudaFreeHost(H->pin_scal);
+    H->pin_scal = nullptr;
+    H->pin_scal_n = 0;
+    HM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&H->pin_scal), need * sizeof(double)));
+    H->pin_scal_n = need;
+  }
+  double* hs = H->pin_scal;  // [0,R) rs_next, [R,2R) alpha, [2R,3R) scratch
+  HM_CUDA(cudaMemcpyAsync(db.get(), B, sizeof(double) * n * R, cudaMemcpyHostToDevice, s));
+  dx.zero(s);
+  HM_CUDA(cudaMemcpyAsync(dr.get(), db.get(), sizeof(double) * n * R, cudaMemcpyDeviceToDevice, s));
+  HM_CUDA(cudaMemcpyAsync(dp.get(), db.get(), sizeof(double) * n * R, cudaMemcpyDeviceToDevice, s));
+  device_dots(db.get(), db.get(), n, Ri, part, bn2, s);
+  device_dots(dr.get(), dr.get(), n, Ri, part, rs, s);
+  std::vector<double> bn(R), rs_host(R);
+  std::vector<int> active(R, 1);
+  HM_CUDA(cudaMemcpyAsync(hs, bn2, sizeof(double) * R, cudaMemcpyDeviceToHost, s));
+  HM_CUDA(cudaMemcpyAsync(hs + R, rs, sizeof(double) * R, cudaMemcpyDeviceToHost, s));
+  HM_CUDA(cudaStreamSynchronize(s));
+  for (long long r = 0; r < R; ++r) {
+    iterations[r] = 0;
+    rel_res[r] = 0.0;
+    bn[r] = std::sqrt(hs[r]);
+    rs_host[r] = hs[R + r];
+    if (bn[r] == 0.0) active[r] = 0;  // zero rhs: zero solution, no iterations
+  }
+  HM_CUDA(cudaMemcpyAsync(act.get(), active.data(), sizeof(int) * R, cudaMemcpyHostToDevice, s));
+  const unsigned gx = grid_for(n, 256, 4096);
+  const dim3 grid(gx, static_cast<unsigned>(R));
+  auto apply = [&](double* in, double* out) {
+    if (multi) product_multi_all(H, in, out, R, flags, s);
+    else product(H, in, out, s);
+    axpy_sigma_kernel<<<grid, 256, 0, s>>>(out, in, sigma2, n);
+    HM_LAUNCH_CHECK();
+  };
+  bool any = std::any_of(active.begin(), active.end(), [](int c) { return c != 0; });
+  for (long long iter = 1; iter <= max_iter && any; ++iter) {
+    apply(dp.get(), dap.get());
+    device_dots(dp.get(), dap.get(), n, Ri, part, pap, s);
+    cg_alpha_kernel<<<(Ri + 31) / 32, 32, 0, s>>>(rs, pap, act.get(), alpha, Ri);
+    cg_update_kernel<<<grid, 256, 0, s>>>(dx.get(), dr.get(), dp.get(), dap.get(), alpha, act.get(), n);
+    HM_LAUNCH_CHECK();
+    device_dots(dr.get(), dr.get(), n, Ri, part, rsn, s);
+    HM_CUDA(cudaMemcpyAsync(hs, rsn, sizeof(double) * R, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaMemcpyAsync(hs + R, alpha, sizeof(double) * R, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+    any = false;
+    bool changed = false;
+    for (long long r = 0; r < R; ++r) {
+      if (!active[r]) continue;
+      const double rs_next = hs[r], a = hs[R + r];
+      if (!std::isfinite(rs_next) || !std::isfinite(a))
+        raise(kEnonfinite, "cg_solve: non-finite value at iteration " + std::to_string(iter) +
+                               (R > 1 ? " (rhs " + std::to_string(r) + ")" : std::string()) + " (residual " +
+                               std::to_string(std::sqrt(std::fabs(rs_host[r])) / bn[r]) + ")");
+      iterations[r] = iter;
+      if (std::sqrt(rs_next) <= tol * bn[r]) {
+        active[r] = 0;
+        changed = true;
+        continue;
+      }
+      rs_host[r] = rs_next;
+      any = true;
+    }
+    if (changed) HM_CUDA(cudaMemcpyAsync(act.get(), active.data(), sizeof(int) * R, cudaMemcpyHostToDevice, s));
+    if (!any) break;
+    cg_beta_kernel<<<(Ri + 31) / 32, 32, 0, s>>>(rs, rsn, act.get(), beta, Ri);
+    cg_dir_kernel<<<grid, 256, 0, s>>>(dp.get(), dr.get(), beta, act.get(), n);
+    HM_LAUNCH_CHECK();
+  }
+  // true residual of the returned iterates (solver.cpp:64-71), on the device
+  apply(dx.get(), dap.get());
+  sub_kernel<<<grid_for(n * R, 256, 1 << 16), 256, 0, s>>>(dap.get(), db.get(), n * R);  // dap = b - A x
+  HM_LAUNCH_CHECK();
+  device_dots(dap.get(), dap.get(), n, Ri, part, pap, s);
+  HM_CUDA(cudaMemcpyAsync(hs, pap, sizeof(double) * R, cudaMemcpyDeviceToHost, s));
+  HM_CUDA(cudaMemcpyAsync(X, dx.get(), sizeof(double) * n * R, cudaMemcpyDeviceToHost, s));
+  HM_CUDA(cudaStreamSynchronize(s));
+  for (long long r = 0; r < R; ++r) {
+    if (bn[r] == 0.0) {
+      std::memset(X + r * n, 0, sizeof(double) * n);
+      continue;
+    }
+    rel_res[r] = std::sqrt(hs[r]) / bn[r];
+  }
+}
+
+}  // namespace
+
 hm_status hm_cg_solve(hm_handle* H, const double* b, double sigma2, double tol, int64_t max_iter, double* x,
                       int64_t* iterations, double* rel_res) {
   return guarded([&] {
-    // solver.cpp:19-73
+    if (!H || !b || !x || !iterations || !rel_res) raise(kEinval, "cg_solve: null argument");
     std::lock_guard<std::mutex> lock(H->mu);
-    HMatrix& h = H->h;
-    if (tol <= 0.0) raise(kEinval, "cg_solve: tol must be > 0");
-    if (max_iter < 1) raise(kEinval, "cg_solve: max_iter must be >= 1");
-    if (sigma2 < 0.0) raise(kEinval, "cg_solve: sigma2 must be >= 0");
-    HM_CUDA(cudaSetDevice(h.device));
-    cudaStream_t s = h.stream;
-    const long long n = h.n;
-    DevBuf<double> db, dx, dr, dp, dap, part, alpha;
-    db.alloc(n, s);
-    dx.alloc(n, s);
-    dr.alloc(n, s);
-    dp.alloc(n, s);
-    dap.alloc(n, s);
-    alpha.alloc(1, s);
-    HM_CUDA(cudaMemcpyAsync(db.get(), b, sizeof(double) * n, cudaMemcpyHostToDevice, s));
-    dx.zero(s);
-    *iterations = 0;
-    *rel_res = 0.0;
-    const double b_norm = std::sqrt(device_dot(db.get(), db.get(), n, part, s));
-    if (b_norm == 0.0) {
-      std::memset(x, 0, sizeof(double) * n);
-      return;
-    }
-    HM_CUDA(cudaMemcpyAsync(dr.get(), db.get(), sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-    HM_CUDA(cudaMemcpyAsync(dp.get(), db.get(), sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-    double rs = device_dot(dr.get(), dr.get(), n, part, s);
-    const unsigned grid = grid_for(n, 256, 1 << 16);
-    for (long long iter = 1; iter <= max_iter; ++iter) {
-      product(H, dp.get(), dap.get(), s);
-      axpy_sigma_kernel<<<grid, 256, 0, s>>>(dap.get(), dp.get(), sigma2, n);
-      HM_LAUNCH_CHECK();
-      const double a = rs / device_dot(dp.get(), dap.get(), n, part, s);
-      HM_CUDA(cudaMemcpyAsync(alpha.get(), &a, sizeof(double), cudaMemcpyHostToDevice, s));
-      cg_update_kernel<<<grid, 256, 0, s>>>(dx.get(), dr.get(), dp.get(), dap.get(), alpha.get(), n);
-      HM_LAUNCH_CHECK();
-      const double rs_next = device_dot(dr.get(), dr.get(), n, part, s);
-      if (!std::isfinite(rs_next) || !std::isfinite(a))
-        raise(kEnonfinite, "cg_solve: non-finite value at iteration " + std::to_string(iter) + " (residual " +
-                               std::to_string(std::sqrt(std::fabs(rs)) / b_norm) + ")");
-      *iterations = iter;
-      if (std::sqrt(rs_next) <= tol * b_norm) break;
-      const double beta = rs_next / rs;
-      cg_dir_kernel<<<grid, 256, 0, s>>>(dp.get(), dr.get(), beta, n);
-      HM_LAUNCH_CHECK();
-      rs = rs_next;
-    }
-    // true residual of the returned iterate (solver.cpp:64-71)
-    product(H, dx.get(), dap.get(), s);
-    axpy_sigma_kernel<<<grid, 256, 0, s>>>(dap.get(), dx.get(), sigma2, n);
-    HM_LAUNCH_CHECK();
-    std::vector<double> ax(n);
-    HM_CUDA(cudaMemcpyAsync(ax.data(), dap.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaMemcpyAsync(x, dx.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaStreamSynchronize(s));
-    double diff_sq = 0.0;
-    for (long long i = 0; i < n; ++i) {
-      const double dd = b[i] - ax[i];
-      diff_sq += dd * dd;
-    }
-    *rel_res = std::sqrt(diff_sq) / b_norm;
+    cg_run(H, b, 1, sigma2, tol, max_iter, 0, false, x, iterations, rel_res);
   });
 }
 
@@ -608,100 +745,18 @@ hm_status hm_mvp_multi_device(hm_handle* H, const double* X_dev, double* Z_dev, 
     if (nrhs < 1) raise(kEinval, "mvp_multi: nrhs must be >= 1");
     std::lock_guard<std::mutex> lock(H->mu);
     HM_CUDA(cudaSetDevice(H->h.device));
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : H->h.stream;
-    product_multi_all(H, X_dev, Z_dev, nrhs, flags, s);
+    on_handle_stream(H->h, static_cast<cudaStream_t>(stream),
+                     [&](cudaStream_t s) { product_multi_all(H, X_dev, Z_dev, nrhs, flags, s); });
   });
 }
 
-// nrhs independent cg_solve runs (solver.cpp:19-73) in lock-step: one multi-RHS product
-// per iteration for all vectors; each keeps its own scalars and stopping rule, so with
-// flags = 0 every column follows exactly the single-RHS iteration.
 hm_status hm_cg_solve_multi(hm_handle* H, const double* B, int64_t nrhs, double sigma2, double tol, int64_t max_iter,
                             int32_t flags, double* X, int64_t* iterations, double* rel_res) {
   return guarded([&] {
     if (!H || !B || !X || !iterations || !rel_res) raise(kEinval, "cg_solve_multi: null argument");
     if (nrhs < 1) raise(kEinval, "cg_solve_multi: nrhs must be >= 1");
-    if (tol <= 0.0) raise(kEinval, "cg_solve: tol must be > 0");
-    if (max_iter < 1) raise(kEinval, "cg_solve: max_iter must be >= 1");
-    if (sigma2 < 0.0) raise(kEinval, "cg_solve: sigma2 must be >= 0");
     std::lock_guard<std::mutex> lock(H->mu);
-    HMatrix& h = H->h;
-    HM_CUDA(cudaSetDevice(h.device));
-    cudaStream_t s = h.stream;
-    const long long n = h.n, R = nrhs;
-    DevBuf<double> db, dx, dr, dp, dap, part, alpha;
-    db.alloc(n * R, s);
-    dx.alloc(n * R, s);
-    dr.alloc(n * R, s);
-    dp.alloc(n * R, s);
-    dap.alloc(n * R, s);
-    alpha.alloc(R, s);
-    HM_CUDA(cudaMemcpyAsync(db.get(), B, sizeof(double) * n * R, cudaMemcpyHostToDevice, s));
-    dx.zero(s);
-    HM_CUDA(cudaMemcpyAsync(dr.get(), db.get(), sizeof(double) * n * R, cudaMemcpyDeviceToDevice, s));
-    HM_CUDA(cudaMemcpyAsync(dp.get(), db.get(), sizeof(double) * n * R, cudaMemcpyDeviceToDevice, s));
-    std::vector<double> bn(R), rs(R);
-    std::vector<char> active(R, 1);
-    for (long long r = 0; r < R; ++r) {
-      iterations[r] = 0;
-      rel_res[r] = 0.0;
-      bn[r] = std::sqrt(device_dot(db.get() + r * n, db.get() + r * n, n, part, s));
-      if (bn[r] == 0.0) active[r] = 0;
-      rs[r] = device_dot(dr.get() + r * n, dr.get() + r * n, n, part, s);
-    }
-    const unsigned grid = grid_for(n, 256, 1 << 16);
-    bool any = std::any_of(active.begin(), active.end(), [](char c) { return c != 0; });
-    for (long long iter = 1; iter <= max_iter && any; ++iter) {
-      product_multi_all(H, dp.get(), dap.get(), R, flags, s);
-      any = false;
-      for (long long r = 0; r < R; ++r) {
-        if (!active[r]) continue;
-        double* pr = dp.get() + r * n;
-        double* apr = dap.get() + r * n;
-        axpy_sigma_kernel<<<grid, 256, 0, s>>>(apr, pr, sigma2, n);
-        HM_LAUNCH_CHECK();
-        const double a = rs[r] / device_dot(pr, apr, n, part, s);
-        HM_CUDA(cudaMemcpyAsync(alpha.get() + r, &a, sizeof(double), cudaMemcpyHostToDevice, s));
-        cg_update_kernel<<<grid, 256, 0, s>>>(dx.get() + r * n, dr.get() + r * n, pr, apr, alpha.get() + r, n);
-        HM_LAUNCH_CHECK();
-        const double rs_next = device_dot(dr.get() + r * n, dr.get() + r * n, n, part, s);
-        if (!std::isfinite(rs_next) || !std::isfinite(a))
-          raise(kEnonfinite, "cg_solve: non-finite value at iteration " + std::to_string(iter) + " (rhs " +
-                                 std::to_string(r) + ")");
-        iterations[r] = iter;
-        if (std::sqrt(rs_next) <= tol * bn[r]) {
-          active[r] = 0;
-          continue;
-        }
-        const double beta = rs_next / rs[r];
-        cg_dir_kernel<<<grid, 256, 0, s>>>(pr, dr.get() + r * n, beta, n);
-        HM_LAUNCH_CHECK();
-        rs[r] = rs_next;
-        any = true;
-      }
-    }
-    // true residuals of the returned iterates (solver.cpp:64-71)
-    product_multi_all(H, dx.get(), dap.get(), R, flags, s);
-    for (long long r = 0; r < R; ++r) {
-      axpy_sigma_kernel<<<grid, 256, 0, s>>>(dap.get() + r * n, dx.get() + r * n, sigma2, n);
-      HM_LAUNCH_CHECK();
-    }
-    std::vector<double> ax(n * R);
-    HM_CUDA(cudaMemcpyAsync(ax.data(), dap.get(), sizeof(double) * n * R, cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaMemcpyAsync(X, dx.get(), sizeof(double) * n * R, cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaStreamSynchronize(s));
-    for (long long r = 0; r < R; ++r) {
-      if (bn[r] == 0.0) {
-        std::memset(X + r * n, 0, sizeof(double) * n);
-        continue;
-      }
-      double diff_sq = 0.0;
-      for (long long i = 0; i < n; ++i) {
-        const double dd = B[r * n + i] - ax[r * n + i];
-        diff_sq += dd * dd;
-      }
-      rel_res[r] = std::sqrt(diff_sq) / bn[r];
-    }
+    cg_run(H, B, nrhs, sigma2, tol, max_iter, flags, true, X, iterations, rel_res);
   });
 }
 
@@ -734,6 +789,7 @@ hm_status hm_dump_leaves_csv(hm_handle* H, const char* path) {
 
 hm_status hm_dense_mvp(hm_handle* H, const double* x, double* z) {
   return guarded([&] {
+    if (!H || !x || !z) raise(kEinval, "dense_mvp: null argument");
     std::lock_guard<std::mutex> lock(H->mu);
     HMatrix& h = H->h;
     HM_CUDA(cudaSetDevice(h.device));
@@ -755,13 +811,22 @@ hm_status hm_dense_mvp(hm_handle* H, const double* x, double* z) {
 
 hm_status hm_relative_error(hm_handle* H, const double* x, double* out) {
   // hmatrix.cpp:125-153 without the N limit (the exact product runs on the device)
-  std::vector<double> zh(H->h.n), ze(H->h.n);
-  hm_status st = hm_mvp(H, x, zh.data(), nullptr);
+  if (!H || !x || !out) {
+    g_err = "relative_error: null argument";
+    return HM_EINVAL;
+  }
+  std::vector<double> zh, ze;
+  hm_status st = guarded([&] {
+    zh.resize(H->h.n);
+    ze.resize(H->h.n);
+  });
+  if (st != HM_OK) return st;
+  st = hm_mvp(H, x, zh.data(), nullptr);
   if (st != HM_OK) return st;
   st = hm_dense_mvp(H, x, ze.data());
   if (st != HM_OK) return st;
   double diff_sq = 0.0, ref_sq = 0.0;
-  for (long long i = 0; i < H->h.n; ++i) {
+  for (size_t i = 0; i < zh.size(); ++i) {
     const double d = zh[i] - ze[i];
     diff_sq += d * d;
     ref_sq += ze[i] * ze[i];
@@ -772,6 +837,7 @@ hm_status hm_relative_error(hm_handle* H, const double* x, double* out) {
 
 hm_status hm_get_timings(hm_handle* H, hm_timings* t) {
   return guarded([&] {
+    if (!H || !t) raise(kEinval, "get_timings: null argument");
     const Timings& tm = H->h.tm;
     t->setup_ms = tm.setup_ms;
     t->morton_ms = tm.morton_ms;
@@ -779,12 +845,36 @@ hm_status hm_get_timings(hm_handle* H, hm_timings* t) {
     t->aca_ms = tm.aca_ms;
     t->near_ms = tm.near_ms;
     t->mvp_ms = tm.mvp_ms;
+    t->mvp_dense_ms = tm.mvp_dense_ms;
+    t->mvp_aca_ms = tm.mvp_aca_ms;
   });
 }
 
 hm_status hm_get_stats(hm_handle* H, hm_stats* st) {
   return guarded([&] {
-    const HMatrix& h = H->h;
+    if (!H || !st) raise(kEinval, "get_stats: null argument");
+    std::lock_guard<std::mutex> lock(H->mu);
+    HMatrix& h = H->h;
+    unsigned long long rej[2] = {0, 0};
+    HM_CUDA(cudaSetDevice(h.device));
+    if (h.aca_rej.size() >= 2)
+      HM_CUDA(cudaMemcpyAsync(rej, h.aca_rej.get(), sizeof(rej), cudaMemcpyDeviceToHost, h.stream));
+    HM_CUDA(cudaStreamSynchronize(h.stream));
+    if (!h.cfg.precompute_aca && h.keff_known) {
+      // recompute mode: ranks of the factorisation inside the last product
+      long long lo = 0, hi = 0;
+      if (!h.chunks.empty()) {
+        lo = h.chunks.front().c0;
+        hi = h.chunks.back().c1;
+      }
+      std::vector<int> ke(std::max(hi - lo, 0ll));
+      if (hi > lo) {
+        HM_CUDA(cudaMemcpyAsync(ke.data(), h.k_eff.get() + lo, sizeof(int) * (hi - lo), cudaMemcpyDeviceToHost,
+                                h.stream));
+        HM_CUDA(cudaStreamSynchronize(h.stream));
+      }
+      rank_sums(h, ke.data(), lo, hi);
+    }
     st->n_dense = h.dense.count;
     st->n_aca = h.aca.count;
     st->S_d = h.S_d;
@@ -794,18 +884,23 @@ hm_status hm_get_stats(hm_handle* H, hm_stats* st) {
     st->S_lm = h.S_lm;
     st->S_ln = h.S_ln;
     st->S_d_own = h.S_d_own;
-    st->aca_rejections = h.aca_rejections;
+    st->aca_rejections = static_cast<int64_t>(rej[0]);
+    st->aca_rejected_entries = static_cast<int64_t>(rej[1]);
+    st->S_chain = h.S_chain;
     st->dmax_leaf = h.dmax_leaf;
     st->row_begin = h.row_begin;
     st->row_end = h.row_end;
     st->device_bytes = static_cast<double>(h.dense_vals.bytes() + h.U.bytes() + h.V.bytes() + h.coords.bytes());
     st->S_d_stored = h.S_d_stored;
     st->near_sym = h.near_sym ? 1 : 0;
+    st->n_aca_batches = h.n_batches;
+    st->n_aca_chunks = static_cast<int64_t>(h.chunks.size());
   });
 }
 
 hm_status hm_get_points(hm_handle* H, double* coords, int64_t* perm) {
   return guarded([&] {
+    if (!H || !coords || !perm) raise(kEinval, "get_points: null argument");
     std::lock_guard<std::mutex> lock(H->mu);
     HMatrix& h = H->h;
     HM_CUDA(cudaSetDevice(h.device));
@@ -817,6 +912,7 @@ hm_status hm_get_points(hm_handle* H, double* coords, int64_t* perm) {
 
 hm_status hm_get_codes(hm_handle* H, uint64_t* codes) {
   return guarded([&] {
+    if (!H || !codes) raise(kEinval, "get_codes: null argument");
     std::lock_guard<std::mutex> lock(H->mu);
     HMatrix& h = H->h;
     HM_CUDA(cudaSetDevice(h.device));
@@ -827,6 +923,7 @@ hm_status hm_get_codes(hm_handle* H, uint64_t* codes) {
 
 hm_status hm_get_leaves(hm_handle* H, int32_t which, int64_t* rows4, double* boxes) {
   return guarded([&] {
+    if (!H || !rows4) raise(kEinval, "get_leaves: null argument");
     std::lock_guard<std::mutex> lock(H->mu);
     HMatrix& h = H->h;
     HM_CUDA(cudaSetDevice(h.device));
@@ -857,48 +954,34 @@ hm_status hm_get_leaves(hm_handle* H, int32_t which, int64_t* rows4, double* box
 
 hm_status hm_get_aca(hm_handle* H, int64_t* k_eff, int64_t* row_piv, int64_t* col_piv, double* u, double* v) {
   return guarded([&] {
+    if (!H || !k_eff || !row_piv || !col_piv) raise(kEinval, "get_aca: null argument");
     std::lock_guard<std::mutex> lock(H->mu);
     HMatrix& h = H->h;
     HM_CUDA(cudaSetDevice(h.device));
     cudaStream_t s = h.stream;
     const long long cnt = h.aca.count, kmax = h.cfg.k;
     if (h.cfg.world > 1) raise(kEinval, "hm_get_aca: single-rank handles only");
-    std::vector<long long> uo(cnt + 1, 0), vo(cnt + 1, 0);
-    for (long long b = 0; b < cnt; ++b) {
-      uo[b + 1] = uo[b] + kmax * h.aca.h_m[b];
-      vo[b + 1] = vo[b] + kmax * h.aca.h_n[b];
-    }
+    const std::vector<long long>& uo = h.h_uoff;
+    const std::vector<long long>& vo = h.h_voff;
     std::vector<double> hu, hv;
     if (u || v) {
       hu.resize(uo[cnt]);
       hv.resize(vo[cnt]);
     }
     if (!h.factors_valid) {
-      // recompute mode: factorise into scratch chunk by chunk (introspection only), the
-      // chunks sized like the product's (mvp.cu) so that any N that runs also factorises
-      size_t free_b = 0, total_b = 0;
-      HM_CUDA(cudaMemGetInfo(&free_b, &total_b));
-      const long long budget = std::max<long long>(1ll << 20, std::min<long long>(free_b / 2, 96ll << 30));
-      long long c0 = 0;
-      while (c0 < cnt) {
-        long long c1 = c0, bytes = 0;
-        while (c1 < cnt) {
-          const long long add = 8 * kmax * (h.aca.h_m[c1] + h.aca.h_n[c1]);
-          if (c1 > c0 && bytes + add > budget) break;
-          bytes += add;
-          ++c1;
-        }
-        if (h.U.size() < static_cast<size_t>(uo[c1] - uo[c0])) h.U.alloc(uo[c1] - uo[c0], s);
-        if (h.V.size() < static_cast<size_t>(vo[c1] - vo[c0])) h.V.alloc(vo[c1] - vo[c0], s);
-        compute_aca(h, c0, c1, s);
+      // recompute mode: factorise into the product's chunk workspace chunk by chunk
+      // (introspection only); the same plan as the product, so any N that runs factorises
+      reset_aca_rejections(h, s);
+      for (const AcaChunk& c : h.chunks) {
+        if (h.U.size() < static_cast<size_t>(c.ue - c.ub)) h.U.alloc(c.ue - c.ub, s);
+        if (h.V.size() < static_cast<size_t>(c.ve - c.vb)) h.V.alloc(c.ve - c.vb, s);
+        compute_aca(h, c, s);
+        h.keff_known = true;
         if (u || v) {
-          HM_CUDA(cudaMemcpyAsync(hu.data() + uo[c0], h.U.get(), sizeof(double) * (uo[c1] - uo[c0]),
-                                  cudaMemcpyDeviceToHost, s));
-          HM_CUDA(cudaMemcpyAsync(hv.data() + vo[c0], h.V.get(), sizeof(double) * (vo[c1] - vo[c0]),
-                                  cudaMemcpyDeviceToHost, s));
+          HM_CUDA(cudaMemcpyAsync(hu.data() + c.ub, h.U.get(), sizeof(double) * (c.ue - c.ub), cudaMemcpyDeviceToHost, s));
+          HM_CUDA(cudaMemcpyAsync(hv.data() + c.vb, h.V.get(), sizeof(double) * (c.ve - c.vb), cudaMemcpyDeviceToHost, s));
           HM_CUDA(cudaStreamSynchronize(s));
         }
-        c0 = c1;
       }
     } else if ((u || v) && cnt) {
       HM_CUDA(cudaMemcpyAsync(hu.data(), h.U.get(), sizeof(double) * uo[cnt], cudaMemcpyDeviceToHost, s));
@@ -911,10 +994,6 @@ hm_status hm_get_aca(hm_handle* H, int64_t* k_eff, int64_t* row_piv, int64_t* co
       HM_CUDA(cudaMemcpyAsync(hcp.data(), h.col_piv.get(), sizeof(int) * cnt * kmax, cudaMemcpyDeviceToHost, s));
     }
     HM_CUDA(cudaStreamSynchronize(s));
-    if (!h.factors_valid) {
-      h.U.reset();
-      h.V.reset();
-    }
     for (long long b = 0; b < cnt; ++b) {
       k_eff[b] = hk[b];
       const long long m = h.aca.h_m[b], n = h.aca.h_n[b];

@@ -61,9 +61,34 @@ struct Timings {
   double mvp_ms = 0, mvp_dense_ms = 0, mvp_aca_ms = 0;
 };
 
-struct HMatrix {
+// ACA kernel size classes (aca.cu): windows <= 64..1024, clusters <= 2048/4096, big, CTA
+constexpr int kAcaClasses = 9;
+
+// One factorisation chunk: aca leaves [c0, c1) with host copies of everything the
+// product needs to launch it without reading the device (see HMatrix::chunks).
+struct AcaChunk {
+  long long c0 = 0, c1 = 0;
+  long long row_lo = 0, row_hi = 0;       // rows its leaves touch
+  long long ub = 0, vb = 0, ue = 0, ve = 0;  // factor offsets u_off/v_off at c0 and c1
+  long long ccount[kAcaClasses] = {};     // jobs per size class
+  long long sched_off = 0;                // into sched_jobs / sched_order
+  int max_rows_big = 0;                   // largest m of the big-block class
+};
+
+// Device, streams and events of a handle.  A base class so that it is destroyed AFTER
+// every DevBuf member of HMatrix (their stream-ordered frees are enqueued on `stream`).
+struct HandleStreams {
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;  // every product / setup operation of the handle
+  cudaStream_t aux = nullptr;     // auxiliary stream (near field beside the V^T x fold)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_last = nullptr;  // end of the last work on `stream` (orders caller streams)
+  cudaEvent_t ev_ph[4] = {};      // MvpTimings: near [0,1), far [2,3)
+  void create(int dev);           // streams + events (throws HM_ECUDA)
+  ~HandleStreams();
+};
+
+struct HMatrix : HandleStreams {
   Config cfg;
   KernelParams kp{};
   long long n = 0;
@@ -104,16 +129,28 @@ struct HMatrix {
   bool tma_rows = false;
   bool tma_far = false;  // recompute mode: far-field chunks on the TMA row kernel (U row-tiled)
   DevBuf<int> k_eff, row_piv, col_piv;
-  DevBuf<int> aca_order;    // aca leaves by column count n, largest first
-  long long aca_long_jobs = 0;  // prefix of aca_order with n >= 2048 (CTA-per-block fold path)
-  cudaStream_t aux = nullptr;   // auxiliary stream (long folds run beside the short ones)
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // host copies of the factor offsets (fixed at setup: the product never reads them back)
+  std::vector<long long> h_uoff, h_voff;
+  // Factorisation schedule, fixed at setup.  The own admissible leaves are split into
+  // chunks (recompute mode: the factor workspace holds one chunk; precompute: one chunk).
+  // A chunk is a run of whole reference batches (partition_aca_queue, aca.cpp:229-250,
+  // Sigma m <= bs_aca) that fits the workspace budget.  Per chunk the leaves are sorted
+  // once into the per-size-class job lists of the ACA kernels (sched_jobs) and the
+  // long-leaves-first order of the V^T x fold (sched_order).
+  std::vector<AcaChunk> chunks;
+  long long n_batches = 0;      // reference batches of the own admissible leaves
+  DevBuf<int> sched_jobs, sched_order;
+  DevBuf<int> aca_counters;     // per-class job counters (reset before every chunk)
+  DevBuf<double> aca_big_scratch;  // window scratch of the big-block ACA kernel (grown once)
+  DevBuf<unsigned long long> aca_rej;  // [0] rejected columns, [1] their entries: current factorisation
+  bool keff_known = false;      // k_eff holds the ranks of a complete factorisation of the own leaves
+  bool phase_events = false;      // record ev_ph around the product phases (hm_mvp)
   DevBuf<double> t;         // per (aca leaf, rank) V^T x
   bool factors_valid = false;
-  long long aca_rejections = 0;
 
   // stored near field: column-major blocks
   DevBuf<long long> dense_off;
+  long long h_dense_off_base = 0;  // dense_off of the first own leaf (host copy)
   DevBuf<double> dense_vals;
   // Symmetric near field (regular geometry, TMA product): A(sigma,tau) = A(tau,sigma)^T
   // bitwise (dx^2 is sign-symmetric), so only blocks with row.lower <= col.lower are
@@ -132,11 +169,13 @@ struct HMatrix {
   // multi-RHS workspaces (multi.cu): rhs-major vectors, chunk-relative t, symmetric partials
   DevBuf<double> xmR, zmR, tR, partR, xinR, zoutR;
   DevBuf<long long> dmma_tiles;
+  long long n_dmma_tiles = -1;  // -1: not built yet
   DevBuf<int> counter;
 
   // algorithmic sizes
   double S_d = 0, sum_m_adm = 0, sum_n_adm = 0, S_l = 0, S_lm = 0, S_ln = 0;
   double S_d_own = 0;  // dense entries of the rows this rank owns
+  double S_chain = 0;  // sum_adm k_eff (k_eff - 1) (m + n), own leaves
   double S_d_stored = 0;  // dense entries stored (near_stored; about S_d_own / 2 when near_sym)
   Timings tm;
   KClock clk;
@@ -158,7 +197,14 @@ void mvp_multi_morton(HMatrix& h, int R, int flags, cudaStream_t s);
 
 // components
 void morton_codes_device(const double* coords, long long n, int d, unsigned long long* codes, cudaStream_t s);
-void compute_aca(HMatrix& h, long long leaf_begin, long long leaf_end, cudaStream_t s);
+// schedule of aca leaves [c0, c1) into h.sched_* at c.sched_off (setup time, may sync)
+void plan_aca_chunk(HMatrix& h, AcaChunk& c, cudaStream_t s);
+// factorise one planned chunk into h.U / h.V (offsets relative to c.ub / c.vb); no host sync
+void compute_aca(HMatrix& h, const AcaChunk& c, cudaStream_t s);
+// rejected-column counter of the current factorisation
+void reset_aca_rejections(HMatrix& h, cudaStream_t s);
+// S_l, S_lm, S_ln, S_chain of the own aca leaves [lo, hi) from their ranks ke[b - lo]
+void rank_sums(HMatrix& h, const int* ke, long long lo, long long hi);
 void store_near_field(HMatrix& h, cudaStream_t s);
 void plan_near_pairs(HMatrix& h, cudaStream_t s);
 void plan_far_field(HMatrix& h, cudaStream_t s);

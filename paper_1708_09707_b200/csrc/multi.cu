@@ -473,19 +473,26 @@ void near_dmma(HMatrix& h, const MArgs& a, cudaStream_t s) {
   const int D = h.dmax_leaf;
   const long long ncl = 1ll << D;
   const long long base = h.depth_base[D];
-  DevBuf<long long> cnt, start;
-  cnt.alloc(ncl + 1, s);
-  start.alloc(ncl + 1, s);
-  tile_count_kernel<<<grid_for(ncl, 256, 1 << 16), 256, 0, s>>>(h.slot_lo.get() + base, h.slot_hi.get() + base, ncl,
-                                                                h.row_begin, h.row_end, cnt.get());
-  HM_LAUNCH_CHECK();
-  const long long ntiles = exclusive_scan_i64(cnt.get(), start.get(), ncl, s);
+  // the tile list depends only on the tree: built by the first DMMA product, then reused
+  if (h.n_dmma_tiles < 0) {
+    DevBuf<long long> cnt, start;
+    cnt.alloc(ncl + 1, s);
+    start.alloc(ncl + 1, s);
+    tile_count_kernel<<<grid_for(ncl, 256, 1 << 16), 256, 0, s>>>(h.slot_lo.get() + base, h.slot_hi.get() + base, ncl,
+                                                                  h.row_begin, h.row_end, cnt.get());
+    HM_LAUNCH_CHECK();
+    const long long nt = exclusive_scan_i64(cnt.get(), start.get(), ncl, s);
+    if (nt > 0) {
+      h.dmma_tiles.alloc(nt, s);
+      tile_fill_kernel<<<grid_for(ncl, 256, 1 << 16), 256, 0, s>>>(h.slot_lo.get() + base, h.slot_hi.get() + base,
+                                                                   ncl, h.row_begin, h.row_end, start.get(),
+                                                                   h.dmma_tiles.get());
+      HM_LAUNCH_CHECK();
+    }
+    h.n_dmma_tiles = nt;
+  }
+  const long long ntiles = h.n_dmma_tiles;
   if (ntiles <= 0) return;
-  if (h.dmma_tiles.size() < static_cast<size_t>(ntiles)) h.dmma_tiles.alloc(ntiles, s);
-  tile_fill_kernel<<<grid_for(ncl, 256, 1 << 16), 256, 0, s>>>(h.slot_lo.get() + base, h.slot_hi.get() + base, ncl,
-                                                               h.row_begin, h.row_end, start.get(),
-                                                               h.dmma_tiles.get());
-  HM_LAUNCH_CHECK();
   const unsigned grid = grid_for(ntiles * 32, 128);
 #define HM_DM(DIM)                                                                                          \
   if (a.R == 8) near_dmma_kernel<DIM, 1><<<grid, 128, 0, s>>>(a, h.dmma_tiles.get(), ntiles);              \
@@ -528,11 +535,9 @@ void mvp_multi_morton(HMatrix& h, int R, int flags, cudaStream_t s) {
       }
       HM_LAUNCH_CHECK();
     }
-    long long ub = 0, vb = 0;
-    HM_CUDA(cudaMemcpyAsync(&ub, h.u_off.get() + alo, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaMemcpyAsync(&vb, h.v_off.get() + alo, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaStreamSynchronize(s));
-    launch_t_multi(h, h.aca_order.get(), ahi - alo, vb, 0, R, s);
+    const AcaChunk c0c = h.chunks.empty() ? AcaChunk{} : h.chunks.front();
+    const long long ub = c0c.ub, vb = c0c.vb;
+    launch_t_multi(h, h.sched_order.get() + c0c.sched_off, ahi - alo, vb, 0, R, s);
     a.a_ubase = ub;
     a.a_lo = alo;
     a.a_hi = ahi;
@@ -543,47 +548,27 @@ void mvp_multi_morton(HMatrix& h, int R, int flags, cudaStream_t s) {
   // recompute mode: near field first (exact rows or DMMA tiles), then ACA chunk by chunk
   if (dmma) near_dmma(h, a, s);
   else dispatch_rows_multi(h, a, near, false, s);
-  size_t free_b = 0, total_b = 0;
-  HM_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  long long budget = h.cfg.aca_chunk_rows > 0 ? h.cfg.aca_chunk_rows * kmax * 16
-                                              : std::max<long long>(static_cast<long long>(h.U.bytes() + h.V.bytes()),
-                                                                std::min<long long>(static_cast<long long>(free_b / 2), 96ll << 30));
-  budget = std::max(budget, 1ll << 20);
-  long long c0 = alo;
-  while (c0 < ahi) {
-    long long c1 = c0, bytes = 0;
-    long long row_hi = 0;  // rows touched by the chunk's leaves (canonical order: from rl[c0])
-    while (c1 < ahi) {
-      const long long add = 8 * kmax * (h.aca.h_m[c1] + h.aca.h_n[c1] + R);
-      if (c1 > c0 && bytes + add > budget) break;
-      bytes += add;
-      row_hi = std::max<long long>(row_hi, static_cast<long long>(h.aca.h_rl[c1]) + h.aca.h_m[c1]);
-      ++c1;
-    }
-    long long ub = 0, vb = 0, ue = 0, ve = 0;
-    HM_CUDA(cudaMemcpyAsync(&ub, h.u_off.get() + c0, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaMemcpyAsync(&vb, h.v_off.get() + c0, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaMemcpyAsync(&ue, h.u_off.get() + c1, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaMemcpyAsync(&ve, h.v_off.get() + c1, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaStreamSynchronize(s));
-    if (h.U.size() < static_cast<size_t>(ue - ub)) h.U.alloc(ue - ub, s);
-    if (h.V.size() < static_cast<size_t>(ve - vb)) h.V.alloc(ve - vb, s);
+  reset_aca_rejections(h, s);
+  for (const AcaChunk& c : h.chunks) {
+    const long long c0 = c.c0, c1 = c.c1;
+    if (h.U.size() < static_cast<size_t>(c.ue - c.ub)) h.U.alloc(c.ue - c.ub, s);
+    if (h.V.size() < static_cast<size_t>(c.ve - c.vb)) h.V.alloc(c.ve - c.vb, s);
     if (h.tR.size() < static_cast<size_t>((c1 - c0) * kmax * R)) h.tR.alloc((c1 - c0) * kmax * R, s);
-    compute_aca(h, c0, c1, s);
-    launch_t_multi(h, h.aca_order.get(), c1 - c0, vb, c0, R, s);
+    compute_aca(h, c, s);
+    launch_t_multi(h, h.sched_order.get() + c.sched_off, c1 - c0, c.vb, c0, R, s);
     MArgs b = base_margs(h, R);
     b.z_acc = 1;
-    b.a_ubase = ub;
+    b.a_ubase = c.ub;
     b.a_lo = c0;
     b.a_hi = c1;
-    b.row_begin = std::max<long long>(h.row_begin, h.aca.h_rl[c0]);
-    b.row_end = std::min<long long>(h.row_end, row_hi);
+    b.row_begin = std::max<long long>(h.row_begin, c.row_lo);
+    b.row_end = std::min<long long>(h.row_end, c.row_hi);
     b.t_base = c0;
     b.U = h.U.get();
     b.t = h.tR.get();
     dispatch_rows_multi(h, b, 0, true, s);
-    c0 = c1;
   }
+  h.keff_known = true;
 }
 
 // workspaces for R right-hand sides (precompute mode: t for every own leaf)

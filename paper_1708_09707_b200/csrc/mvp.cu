@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <limits>
 #include <string>
 #include <vector>
 
@@ -1058,14 +1059,14 @@ __global__ void __launch_bounds__(WARPS * 32) t_pair_kernel(const int* __restric
 }
 
 template <int CH, int NST, int WARPS>
-void launch_pair(HMatrix& h, long long njobs, long long v_base, int max_ctas, cudaStream_t s) {
+void launch_pair(HMatrix& h, const int* order, long long njobs, long long v_base, int max_ctas, cudaStream_t s) {
   constexpr int STAGE = 2 * CH * 16 + 2 * (CH + 2);
   const size_t smem = static_cast<size_t>(WARPS) * NST * (8 + 32) + sizeof(double) * WARPS * NST * STAGE;
   HM_CUDA(cudaFuncSetAttribute(t_pair_kernel<CH, NST, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
   const unsigned grid = static_cast<unsigned>(std::min<long long>((njobs / 2 + WARPS) / WARPS, max_ctas));
   HM_CUDA(cudaMemsetAsync(h.counter.get(), 0, sizeof(int), s));
-  t_pair_kernel<CH, NST, WARPS><<<grid, WARPS * 32, smem, s>>>(h.aca_order.get(), njobs, h.aca.cl.get(),
+  t_pair_kernel<CH, NST, WARPS><<<grid, WARPS * 32, smem, s>>>(order, njobs, h.aca.cl.get(),
                                                               h.aca.n.get(), h.k_eff.get(), h.v_off.get(), v_base,
                                                               h.V.get(), h.xm.get(), h.counter.get(), h.t.get());
   HM_LAUNCH_CHECK();
@@ -1086,7 +1087,7 @@ void launch_fold(HMatrix& h, const int* order, long long njobs, long long v_base
   HM_LAUNCH_CHECK();
 }
 
-void launch_t(HMatrix& h, long long njobs, long long v_base, cudaStream_t s) {
+void launch_t(HMatrix& h, const int* order, long long njobs, long long v_base, cudaStream_t s) {
   if (njobs <= 0) return;
   const int kmax = static_cast<int>(h.cfg.k);
   if (kmax > 32) raise(kEinval, "k > 32 not supported by the low-rank apply");
@@ -1095,17 +1096,17 @@ void launch_t(HMatrix& h, long long njobs, long long v_base, cudaStream_t s) {
     HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h.device));
     if (kmax == 16) {
       // pairs of leaves per warp, 8 warps x 3 stages x 17 KB per CTA -> 1 CTA (8 warps) per SM
-      launch_pair<32, 3, 4>(h, njobs, v_base, sms * 2, s);
+      launch_pair<32, 3, 4>(h, order, njobs, v_base, sms * 2, s);
       return;
     }
-    if (kmax <= 16) launch_fold<32, 3, 8, true>(h, h.aca_order.get(), njobs, v_base, sms * 2, s);
-    else launch_fold<16, 3, 8, true>(h, h.aca_order.get(), njobs, v_base, sms * 2, s);
+    if (kmax <= 16) launch_fold<32, 3, 8, true>(h, order, njobs, v_base, sms * 2, s);
+    else launch_fold<16, 3, 8, true>(h, order, njobs, v_base, sms * 2, s);
     return;
   }
   // odd k: thread-per-(leaf, rank) fallback
   int G = 1;
   while (G < kmax) G <<= 1;
-  lowrank_t_kernel<<<grid_for(njobs * G, 256), 256, 0, s>>>(h.aca_order.get(), njobs, h.aca.cl.get(), h.aca.n.get(),
+  lowrank_t_kernel<<<grid_for(njobs * G, 256), 256, 0, s>>>(order, njobs, h.aca.cl.get(), h.aca.n.get(),
                                                             h.k_eff.get(), h.v_off.get(), v_base, h.V.get(),
                                                             h.xm.get(), kmax, G, h.t.get());
   HM_LAUNCH_CHECK();
@@ -1149,6 +1150,7 @@ void store_near_field(HMatrix& h, cudaStream_t s) {
   }
   off[h.dense.count] = run;
   h.S_d_stored = static_cast<double>(run);
+  h.h_dense_off_base = off[lo];
   h.dense_off.alloc(off.size(), s);
   HM_CUDA(cudaMemcpyAsync(h.dense_off.get(), off.data(), sizeof(long long) * off.size(), cudaMemcpyHostToDevice, s));
   h.dense_vals.alloc(std::max(run, 1ll), s);
@@ -1282,10 +1284,26 @@ void launch_near_pairs(HMatrix& h, cudaStream_t s) {
   HM_LAUNCH_CHECK();
 }
 
-// Allocates offsets and (precompute mode) computes all factors of the own range.
+// S_l = S_lm + S_ln and the chain work S_chain of the own leaves [lo, hi) from k_eff
+void rank_sums(HMatrix& h, const int* ke, long long lo, long long hi) {
+  h.S_l = h.S_lm = h.S_ln = h.S_chain = 0;
+  for (long long b = lo; b < hi; ++b) {
+    const double k = ke[b - lo], m = h.aca.h_m[b], n = h.aca.h_n[b];
+    h.S_lm += k * m;
+    h.S_ln += k * n;
+    h.S_chain += k * (k - 1.0) * (m + n);
+  }
+  h.S_l = h.S_lm + h.S_ln;
+}
+
+// Factor offsets, the chunk/batch plan and the factorisation schedule of the own
+// admissible leaves; in precompute mode also the factors themselves.
 void plan_far_field(HMatrix& h, cudaStream_t s) {
   const long long kmax = h.cfg.k;
-  std::vector<long long> uo(h.aca.count + 1, 0), vo(h.aca.count + 1, 0);
+  std::vector<long long>& uo = h.h_uoff;
+  std::vector<long long>& vo = h.h_voff;
+  uo.assign(h.aca.count + 1, 0);
+  vo.assign(h.aca.count + 1, 0);
   for (long long b = 0; b < h.aca.count; ++b) {
     uo[b + 1] = uo[b] + kmax * h.aca.h_m[b];
     vo[b + 1] = vo[b] + kmax * h.aca.h_n[b];
@@ -1299,6 +1317,7 @@ void plan_far_field(HMatrix& h, cudaStream_t s) {
   h.row_piv.alloc(std::max(h.aca.count * kmax, 1ll), s);
   h.col_piv.alloc(std::max(h.aca.count * kmax, 1ll), s);
   h.t.alloc(std::max(h.aca.count * kmax, 1ll), s);
+  reset_aca_rejections(h, s);
   long long lo, hi;
   own_range(h.aca, h.row_begin, h.row_end, lo, hi);
   {
@@ -1317,6 +1336,63 @@ void plan_far_field(HMatrix& h, cudaStream_t s) {
       h.u_tile_shift = sh;
     }
   }
+  // Reference batches (partition_aca_queue, aca.cpp:229-250): greedy in leaf order,
+  // closed before a block that would push Sigma m past bs_aca (bs_aca <= 0: one block per
+  // batch).  Device chunks are runs of whole batches within the factor workspace budget
+  // (precompute: everything; recompute: aca_chunk_rows rows, or half the free HBM up to
+  // 96 GB).  Results do not depend on either partition (per-block ACA is independent).
+  long long budget = std::numeric_limits<long long>::max();
+  if (!h.cfg.precompute_aca) {
+    size_t free_b = 0, total_b = 0;
+    HM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    budget = h.cfg.aca_chunk_rows > 0 ? h.cfg.aca_chunk_rows * kmax * 16
+                                      : std::min<long long>(static_cast<long long>(free_b / 2), 96ll << 30);
+    budget = std::max(budget, 1ll << 20);
+  }
+  h.chunks.clear();
+  h.n_batches = 0;
+  {
+    AcaChunk cur;
+    cur.c0 = cur.c1 = lo;
+    long long cbytes = 0;
+    long long b = lo;
+    while (b < hi) {
+      // next reference batch [b, e)
+      long long e = b, rows = 0, bytes = 0;
+      while (e < hi) {
+        const long long m = h.aca.h_m[e];
+        if (e > b && (h.cfg.bs_aca <= 0 || rows + m > h.cfg.bs_aca)) break;
+        rows += m;
+        bytes += 8 * kmax * (h.aca.h_m[e] + h.aca.h_n[e]);
+        ++e;
+      }
+      ++h.n_batches;
+      if (cur.c1 > cur.c0 && cbytes + bytes > budget) {
+        h.chunks.push_back(cur);
+        cur = AcaChunk{};
+        cur.c0 = cur.c1 = b;
+        cbytes = 0;
+      }
+      cur.c1 = e;
+      cbytes += bytes;
+      b = e;
+    }
+    if (cur.c1 > cur.c0) h.chunks.push_back(cur);
+  }
+  h.sched_jobs.alloc(std::max(hi - lo, 1ll), s);
+  h.sched_order.alloc(std::max(hi - lo, 1ll), s);
+  for (AcaChunk& c : h.chunks) {
+    c.sched_off = c.c0 - lo;
+    c.ub = uo[c.c0];
+    c.vb = vo[c.c0];
+    c.ue = uo[c.c1];
+    c.ve = vo[c.c1];
+    c.row_lo = h.aca.h_rl[c.c0];
+    c.row_hi = 0;
+    for (long long b = c.c0; b < c.c1; ++b)
+      c.row_hi = std::max<long long>(c.row_hi, static_cast<long long>(h.aca.h_rl[b]) + h.aca.h_m[b]);
+    plan_aca_chunk(h, c, s);
+  }
   if (h.cfg.precompute_aca) {
     const auto t0 = std::chrono::steady_clock::now();
     h.U.alloc(std::max(uo[hi] - uo[lo], 1ll), s);
@@ -1326,39 +1402,30 @@ void plan_far_field(HMatrix& h, cudaStream_t s) {
       std::fprintf(stderr, "[hm_trace] U/V alloc %.1f GB: %.3f ms\n", 8.0 * (uo[hi] - uo[lo] + vo[hi] - vo[lo]) / 1e9,
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     }
-    compute_aca(h, lo, hi, s);
+    for (const AcaChunk& c : h.chunks) compute_aca(h, c, s);
     h.factors_valid = true;
     // S_l with the achieved ranks
     std::vector<int> ke(hi - lo);
     if (hi > lo) HM_CUDA(cudaMemcpyAsync(ke.data(), h.k_eff.get() + lo, sizeof(int) * (hi - lo), cudaMemcpyDeviceToHost, s));
     HM_CUDA(cudaStreamSynchronize(s));
-    h.S_l = h.S_lm = h.S_ln = 0;
-    for (long long b = lo; b < hi; ++b) {
-      h.S_lm += static_cast<double>(ke[b - lo]) * h.aca.h_m[b];
-      h.S_ln += static_cast<double>(ke[b - lo]) * h.aca.h_n[b];
-    }
-    h.S_l = h.S_lm + h.S_ln;
+    h.keff_known = true;
+    rank_sums(h, ke.data(), lo, hi);
   }
 }
 
+static void phase_mark(HMatrix& h, int i, cudaStream_t s) {
+  if (h.phase_events) HM_CUDA(cudaEventRecord(h.ev_ph[i], s));
+}
+
+// Stream-ordered: every offset the launches need is a host copy made at setup, so the
+// product never synchronises (it can be captured into a CUDA graph).
 void mvp_morton(HMatrix& h, cudaStream_t s) {
   RowArgs a = base_row_args(h);
   const int near = h.cfg.near_stored ? 2 : 1;
-  long long alo, ahi, dlo, dhi;
-  own_range(h.aca, h.row_begin, h.row_end, alo, ahi);
-  own_range(h.dense, h.row_begin, h.row_end, dlo, dhi);
-  a.d_off_base = 0;
-  if (h.cfg.near_stored) {
-    long long ob = 0;
-    HM_CUDA(cudaMemcpyAsync(&ob, h.dense_off.get() + dlo, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaStreamSynchronize(s));
-    a.d_off_base = ob;
-  }
+  a.d_off_base = h.cfg.near_stored ? h.h_dense_off_base : 0;
   if (h.cfg.precompute_aca) {
-    long long ub = 0, vb = 0;
-    HM_CUDA(cudaMemcpyAsync(&ub, h.u_off.get() + alo, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaMemcpyAsync(&vb, h.v_off.get() + alo, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaStreamSynchronize(s));
+    const bool have = !h.chunks.empty();
+    const AcaChunk c = have ? h.chunks.front() : AcaChunk{};
     // the near-field pair kernel and the V^T x fold are independent HBM streams: run
     // them concurrently (auxiliary stream) so each fills the other's ramp and tail
     // (serial while the per-kernel event clock is on, so each kernel's time is its own)
@@ -1370,20 +1437,25 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
         HM_CUDA(cudaStreamWaitEvent(h.aux, h.ev_fork, 0));
         sn = h.aux;
       }
+      phase_mark(h, 0, sn);
       h.clk.start(kKNearPairs, sn);
       if ((h.n >> h.dmax_leaf) == 64) launch_near_pairs<64>(h, sn);
       else launch_near_pairs<32>(h, sn);
       h.clk.stop(kKNearPairs, sn);
+      phase_mark(h, 1, sn);
       if (near_par) HM_CUDA(cudaEventRecord(h.ev_join, h.aux));
+    } else {
+      phase_mark(h, 0, s);
+      phase_mark(h, 1, s);
     }
-    // aca_order covers [alo, ahi) from the precompute
+    phase_mark(h, 2, s);
     h.clk.start(kKLowrankT, s);
-    launch_t(h, ahi - alo, vb, s);
+    if (have) launch_t(h, h.sched_order.get() + c.sched_off, c.c1 - c.c0, c.vb, s);
     h.clk.stop(kKLowrankT, s);
     if (near_par) HM_CUDA(cudaStreamWaitEvent(s, h.ev_join, 0));
-    a.a_ubase = ub;
-    a.a_lo = alo;
-    a.a_hi = ahi;
+    a.a_ubase = c.ub;
+    a.a_lo = c.c0;
+    a.a_hi = c.c1;
     h.clk.start(kKRows, s);
     if (h.tma_rows) {
       TmaArgs A;
@@ -1408,9 +1480,11 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
       dispatch_rows(h, a, near, true, s);
     }
     h.clk.stop(kKRows, s);
+    phase_mark(h, 3, s);
     return;
   }
   // recompute mode (reference default): near field first, then ACA chunk by chunk
+  phase_mark(h, 0, s);
   h.clk.start(kKRows, s);
   if (h.near_sym_rc && near == 1) {
     if (h.n_pairs > 0) {
@@ -1422,57 +1496,38 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
     dispatch_rows(h, a, near, false, s);
   }
   h.clk.stop(kKRows, s);
+  phase_mark(h, 1, s);
+  phase_mark(h, 2, s);
   const long long kmax = h.cfg.k;
-  // chunk budget: U+V bytes
-  size_t free_b = 0, total_b = 0;
-  HM_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  long long budget = h.cfg.aca_chunk_rows > 0 ? h.cfg.aca_chunk_rows * kmax * 16
-                                              : std::max<long long>(static_cast<long long>(h.U.bytes() + h.V.bytes()),
-                                                                std::min<long long>(static_cast<long long>(free_b / 2), 96ll << 30));
-  budget = std::max(budget, 1ll << 20);
-  long long c0 = alo;
-  while (c0 < ahi) {
-    long long c1 = c0, bytes = 0;
-    long long row_hi = 0;  // rows touched by the chunk's leaves (canonical order: from rl[c0])
-    while (c1 < ahi) {
-      const long long add = 8 * kmax * (h.aca.h_m[c1] + h.aca.h_n[c1]);
-      if (c1 > c0 && bytes + add > budget) break;
-      bytes += add;
-      row_hi = std::max<long long>(row_hi, static_cast<long long>(h.aca.h_rl[c1]) + h.aca.h_m[c1]);
-      ++c1;
-    }
-    long long ub = 0, vb = 0, ue = 0, ve = 0;
-    HM_CUDA(cudaMemcpyAsync(&ub, h.u_off.get() + c0, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaMemcpyAsync(&vb, h.v_off.get() + c0, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaMemcpyAsync(&ue, h.u_off.get() + c1, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaMemcpyAsync(&ve, h.v_off.get() + c1, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaStreamSynchronize(s));
-    const bool trace = std::getenv("HM_TRACE") != nullptr;
+  const bool trace = std::getenv("HM_TRACE") != nullptr;
+  reset_aca_rejections(h, s);
+  for (const AcaChunk& c : h.chunks) {
     const auto tc0 = std::chrono::steady_clock::now();
-    if (h.U.size() < static_cast<size_t>(ue - ub)) h.U.alloc(ue - ub, s);
-    if (h.V.size() < static_cast<size_t>(ve - vb)) h.V.alloc(ve - vb, s);
+    // the workspace is allocated by the first product and reused
+    if (h.U.size() < static_cast<size_t>(c.ue - c.ub)) h.U.alloc(c.ue - c.ub, s);
+    if (h.V.size() < static_cast<size_t>(c.ve - c.vb)) h.V.alloc(c.ve - c.vb, s);
     const auto tc1 = std::chrono::steady_clock::now();
     h.clk.start(kKAca, s);
-    compute_aca(h, c0, c1, s);
+    compute_aca(h, c, s);
     h.clk.stop(kKAca, s);
     if (trace) {
       HM_CUDA(cudaStreamSynchronize(s));
       const auto tc2 = std::chrono::steady_clock::now();
-      std::fprintf(stderr, "[hm_trace] chunk [%lld,%lld) %.1f GB: alloc %.1f ms, aca (host wall) %.1f ms\n", c0, c1,
-                   bytes / 1e9, std::chrono::duration<double, std::milli>(tc1 - tc0).count(),
+      std::fprintf(stderr, "[hm_trace] chunk [%lld,%lld) %.1f GB: alloc %.1f ms, aca (host wall) %.1f ms\n", c.c0, c.c1,
+                   8.0 * (c.ue - c.ub + c.ve - c.vb) / 1e9, std::chrono::duration<double, std::milli>(tc1 - tc0).count(),
                    std::chrono::duration<double, std::milli>(tc2 - tc1).count());
     }
     h.clk.start(kKLowrankT, s);
-    launch_t(h, c1 - c0, vb, s);
+    launch_t(h, h.sched_order.get() + c.sched_off, c.c1 - c.c0, c.vb, s);
     h.clk.stop(kKLowrankT, s);
     RowArgs b = base_row_args(h);
     b.z_in = h.zm.get();
-    b.a_ubase = ub;
-    b.a_lo = c0;
-    b.a_hi = c1;
+    b.a_ubase = c.ub;
+    b.a_lo = c.c0;
+    b.a_hi = c.c1;
     // only the rows the chunk's leaves touch (the others keep their partial sums)
-    b.row_begin = std::max<long long>(h.row_begin, h.aca.h_rl[c0]);
-    b.row_end = std::min<long long>(h.row_end, row_hi);
+    b.row_begin = std::max<long long>(h.row_begin, c.row_lo);
+    b.row_end = std::min<long long>(h.row_end, c.row_hi);
     h.clk.start(kKRowsFar, s);
     if (h.tma_far) {
       const long long S = h.n >> h.dmax_leaf;
@@ -1496,8 +1551,9 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
       dispatch_rows(h, b, 0, true, s);
     }
     h.clk.stop(kKRowsFar, s);
-    c0 = c1;
   }
+  h.keff_known = true;
+  phase_mark(h, 3, s);
 }
 
 void mvp_device(HMatrix& h, const double* x_dev, double* z_dev, cudaStream_t s) {

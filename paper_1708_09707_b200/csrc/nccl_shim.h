@@ -20,6 +20,7 @@ struct NcclApi {
   decltype(&ncclGroupStart) GroupStart = nullptr;
   decltype(&ncclGroupEnd) GroupEnd = nullptr;
   decltype(&ncclBroadcast) Broadcast = nullptr;
+  decltype(&ncclAllGather) AllGather = nullptr;
 
   static const NcclApi& get() {
     static NcclApi api = load();
@@ -39,7 +40,9 @@ struct NcclApi {
     a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(h, "ncclGroupStart"));
     a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
     a.Broadcast = reinterpret_cast<decltype(a.Broadcast)>(dlsym(h, "ncclBroadcast"));
-    if (!a.CommInitRank || !a.CommDestroy || !a.GroupStart || !a.GroupEnd || !a.Broadcast) a.GetUniqueId = nullptr;
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
+    if (!a.CommInitRank || !a.CommDestroy || !a.GroupStart || !a.GroupEnd || !a.Broadcast || !a.AllGather)
+      a.GetUniqueId = nullptr;
     return a;
   }
 };

@@ -187,8 +187,24 @@ __global__ void radix_scatter_kernel(const unsigned long long* __restrict__ keys
 
 }  // namespace
 
+void exclusive_scan_i64_async(const long long* in, long long* out, long long n, long long* total_dev,
+                              cudaStream_t s);
+
 long long exclusive_scan_i64(const long long* in, long long* out, long long n, cudaStream_t s) {
   if (n <= 0) return 0;
+  DevBuf<long long> tot;
+  tot.alloc(1, s);
+  exclusive_scan_i64_async(in, out, n, tot.get(), s);
+  long long total = 0;
+  HM_CUDA(cudaMemcpyAsync(&total, tot.get(), sizeof(long long), cudaMemcpyDeviceToHost, s));
+  HM_CUDA(cudaStreamSynchronize(s));
+  return total;
+}
+
+// stream-ordered scan; the grand total (if total_dev) stays on the device
+void exclusive_scan_i64_async(const long long* in, long long* out, long long n, long long* total_dev,
+                              cudaStream_t s) {
+  if (n <= 0) return;
   const long long nb = (n + kScanTile - 1) / kScanTile;
   DevBuf<long long> sums;
   sums.alloc(static_cast<size_t>(nb + 1), s);
@@ -198,10 +214,8 @@ long long exclusive_scan_i64(const long long* in, long long* out, long long n, c
   HM_LAUNCH_CHECK();
   scan_apply_kernel<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, out, n, sums.get());
   HM_LAUNCH_CHECK();
-  long long total = 0;
-  HM_CUDA(cudaMemcpyAsync(&total, sums.get() + nb, sizeof(long long), cudaMemcpyDeviceToHost, s));
-  HM_CUDA(cudaStreamSynchronize(s));
-  return total;
+  if (total_dev)
+    HM_CUDA(cudaMemcpyAsync(total_dev, sums.get() + nb, sizeof(long long), cudaMemcpyDeviceToDevice, s));
 }
 
 void iota_u32(unsigned* out, long long n, cudaStream_t s) {
@@ -239,7 +253,7 @@ void radix_sort_pairs(unsigned long long* keys, unsigned* vals, long long n, cud
     if (((varying >> shift) & 255ull) == 0) continue;
     radix_hist_kernel<<<static_cast<unsigned>(ntiles), kSortThreads, 0, s>>>(kin, n, shift, ntiles, hist.get());
     HM_LAUNCH_CHECK();
-    exclusive_scan_i64(hist.get(), hist.get(), 256 * ntiles, s);
+    exclusive_scan_i64_async(hist.get(), hist.get(), 256 * ntiles, nullptr, s);  // no host sync per pass
     radix_scatter_kernel<<<static_cast<unsigned>(ntiles), kSortThreads, 0, s>>>(kin, vin, kout, vout, n, shift,
                                                                              ntiles, hist.get());
     HM_LAUNCH_CHECK();

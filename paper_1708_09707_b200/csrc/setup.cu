@@ -423,8 +423,31 @@ void morton_codes_device(const double* coords, long long n, int d, unsigned long
   HM_LAUNCH_CHECK();
 }
 
-HMatrix::~HMatrix() {
+void HandleStreams::create(int dev) {
+  device = dev;
+  HM_CUDA(cudaSetDevice(dev));
+  HM_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  HM_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+  HM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+  HM_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  HM_CUDA(cudaEventCreateWithFlags(&ev_last, cudaEventDisableTiming));
+  for (cudaEvent_t& e : ev_ph) HM_CUDA(cudaEventCreate(&e));
+}
+
+HandleStreams::~HandleStreams() {
+  cudaSetDevice(device);
   if (stream) cudaStreamSynchronize(stream);
+  if (aux) cudaStreamSynchronize(aux);
+  if (stream) cudaStreamDestroy(stream);
+  if (aux) cudaStreamDestroy(aux);
+  for (cudaEvent_t e : {ev_fork, ev_join, ev_last, ev_ph[0], ev_ph[1], ev_ph[2], ev_ph[3]})
+    if (e) cudaEventDestroy(e);
+}
+
+HMatrix::~HMatrix() {
+  cudaSetDevice(device);
+  if (stream) cudaStreamSynchronize(stream);
+  if (aux) cudaStreamSynchronize(aux);
 }
 
 void build_hmatrix(HMatrix& h, const double* coords_in) {

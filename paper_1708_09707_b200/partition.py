@@ -37,3 +37,24 @@ def straddling_leaves(rows4, n: int, world: int):
                 bad.append((rl, ru, cl, cu))
                 break
     return bad
+
+
+def allgather_rows(mine, n: int, world: int, rank: int, group=None):
+    """Host-transport allgather of the y row slices (the gloo / CPU path of the NCCL
+    y-allgather in hm_api.cu, allgather_y): every rank contributes its Morton rows
+    [lo, hi) of row_slices(n, world) and receives the full Morton-ordered vector.
+    Slices may differ by one row (ceil splits): they are padded to the widest."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    bounds = row_slices(n, world)
+    lo, hi = bounds[rank]
+    mine = np.asarray(mine, dtype=np.float64)
+    if mine.shape != (hi - lo,):
+        raise ValueError("allgather_rows: slice length does not match the rank's rows")
+    width = max(b - a for a, b in bounds)
+    padded = torch.zeros(width, dtype=torch.float64)
+    padded[: hi - lo] = torch.from_numpy(mine)
+    gathered = [torch.empty(width, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(gathered, padded, group=group)
+    return np.concatenate([gathered[r][: b - a].numpy() for r, (a, b) in enumerate(bounds)])

@@ -33,18 +33,8 @@ def _worker(rank, world, port, n, d, out_path):
     lo, hi = row_slices(n, world)[rank]
     x = symmetric(7, n)
     zm = h.mvp_rows(x, [(lo, hi)])
-    mine = torch.from_numpy(zm[lo:hi].copy())
-    sizes = [b - a for a, b in row_slices(n, world)]
-    parts = [torch.empty(s, dtype=torch.float64) for s in sizes]
-    # all_gather needs equal sizes: gather padded slices
-    width = max(sizes)
-    padded = torch.zeros(width, dtype=torch.float64)
-    padded[: hi - lo] = mine
-    gathered = [torch.empty(width, dtype=torch.float64) for _ in range(world)]
-    dist.all_gather(gathered, padded)
-    for r in range(world):
-        parts[r] = gathered[r][: sizes[r]]
-    full_m = torch.cat(parts).numpy()
+    from paper_1708_09707_b200.partition import allgather_rows
+    full_m = allgather_rows(zm[lo:hi], n, world, rank)
     _, perm = h.points()
     z = np.empty(n)
     z[perm] = full_m
