@@ -92,6 +92,8 @@ typedef struct {
   int64_t n_aca_chunks;    /* device factorisation chunks (runs of whole batches) */
   int64_t aca_rejected_entries; /* sum of m over the rejected candidate columns (last factorisation) */
   double S_chain;          /* sum_adm k_eff (k_eff - 1) (m + n): residual-chain FP64 ops, own rows */
+  int64_t near_pairs;      /* symmetric near field: dense blocks evaluated/streamed once for both leaves */
+  int32_t near_sym_rc;     /* 1: recomputed near field on the symmetric pair kernel */
 } hm_stats;
 
 const char* hm_last_error(void);
@@ -110,7 +112,9 @@ void hm_destroy(hm_handle* h);
 /* hmat::mvp(HMatrix, x, kernel, MvpTimings*) -- hmatrix.hpp:58-59.  Host x and z
  * (length n, original ordering); copies are inside the call. */
 hm_status hm_mvp(hm_handle* h, const double* x, double* z, hm_timings* t);
-/* Device x and z on `stream` (cudaStream_t; NULL = the handle's stream).  Asynchronous:
+/* Device x and z on `stream` (cudaStream_t; NULL = the legacy default stream, as in the
+ * CUDA runtime).  The product runs on the handle's stream, ordered after the work already
+ * queued on `stream`, and `stream` is ordered after the product.  Asynchronous:
  * no host synchronisation (every launch parameter is fixed at setup), so the call can be
  * captured into a CUDA graph on `stream` once a first product has sized the workspaces. */
 hm_status hm_mvp_device(hm_handle* h, const double* x_dev, double* z_dev, void* stream);

@@ -443,4 +443,66 @@ int ref_mvp_rows_timed(void* h, const double* x, std::int64_t nranges, const std
   });
 }
 
+// Reference CPU arm for the recompute-mode (matrix-free) configurations, where the
+// reference's own setup() at N = 2^22 is far outside a bench's time budget: the
+// reference's recompute-mode mvp() body (hmatrix.cpp:80-113, with aca_batched inside
+// the product, :96-104) over an explicit sample of leaves of the (bit-verified) block
+// tree, on the Morton-ordered points.  Per rep: dense groups assembled and applied,
+// then ACA batches factorised and applied -- exactly the work mvp() does per leaf.
+// t_ms = total over reps; flops = 2 (sum_dense m n + sum_adm k_eff (m + n)) per rep.
+int ref_leaves_mvp_timed(const double* coords_m, std::int64_t n, int d, int kernel, double beta, std::int64_t k,
+                         double eta, std::int64_t ndense, const std::int64_t* dense4, std::int64_t naca,
+                         const std::int64_t* aca4, const double* xm, std::int64_t reps, double* z_morton,
+                         double* t_ms, double* flops) {
+  return guarded([&] {
+    using Clock = std::chrono::steady_clock;
+    const PointSet pts = make_points(n, d, coords_m, nullptr);
+    const KernelFunction kf = make_kernel(kernel, beta);
+    auto items = [&](std::int64_t cnt, const std::int64_t* r4, bool adm) {
+      std::vector<WorkItem> v(static_cast<std::size_t>(cnt));
+      for (std::int64_t i = 0; i < cnt; ++i) {
+        v[i].row = Cluster{r4[4 * i], r4[4 * i + 1]};
+        v[i].col = Cluster{r4[4 * i + 2], r4[4 * i + 3]};
+        v[i].admissible = adm;
+      }
+      return v;
+    };
+    const std::vector<WorkItem> dense = items(ndense, dense4, false), aca = items(naca, aca4, true);
+    AcaOptions opt;
+    opt.max_rank = k;
+    opt.eta = eta;
+    const std::vector<DenseGroup> groups = partition_dense_queue(dense, std::int64_t{1} << 22);
+    const std::vector<AcaBatch> batches = partition_aca_queue(aca, std::int64_t{1} << 20);
+    const std::span<const double> x{xm, static_cast<std::size_t>(n)};
+    double f = 0.0;
+    for (const WorkItem& w : dense) f += 2.0 * static_cast<double>(w.row.size()) * static_cast<double>(w.col.size());
+    const auto t0 = Clock::now();
+    for (std::int64_t rep = 0; rep < reps; ++rep) {
+      std::fill(z_morton, z_morton + n, 0.0);
+      DenseBatch dbatch;
+      std::vector<double> y;
+      for (const DenseGroup& g : groups) {
+        assemble_dense_batch(g, kf, pts, dbatch);
+        gather_dense_inputs(dbatch, x);
+        batched_gemv(dbatch, y);
+        for (std::size_t b = 0; b < g.items.size(); ++b)
+          for (std::int64_t i = 0; i < g.items[b].row.size(); ++i) z_morton[g.items[b].row.lower + i] += y[g.row_offset[b] + i];
+      }
+      for (const AcaBatch& batch : batches) {
+        const BatchedAcaResult res = aca_batched(batch, kf, pts, opt);
+        if (rep == 0)
+          for (std::size_t b = 0; b < batch.items.size(); ++b)
+            f += 2.0 * static_cast<double>(res.k_eff[b]) *
+                 static_cast<double>(batch.items[b].row.size() + batch.items[b].col.size());
+        y.assign(static_cast<std::size_t>(batch.total_rows), 0.0);
+        batched_low_rank_apply(res, batch, x, y);
+        for (std::size_t b = 0; b < batch.items.size(); ++b)
+          for (std::int64_t i = 0; i < batch.items[b].row.size(); ++i) z_morton[batch.items[b].row.lower + i] += y[batch.row_offset[b] + i];
+      }
+    }
+    *t_ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+    *flops = f;
+  });
+}
+
 }  // extern "C"

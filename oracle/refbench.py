@@ -78,8 +78,38 @@ def worker(args) -> dict:
             "t_setup_ms": t_setup, "rows": rows, "clusters": ids, "threads": int(L.ref_threads())}
 
 
+def leaves_worker(args) -> dict:
+    """Recompute-mode sample: the reference's mvp() body with ACA inside the product over
+    the explicit leaf sample in args.leaves (npz written by bench.py; see
+    ref_leaves_mvp_timed in ref_driver.cpp)."""
+    os.environ.setdefault("HMAT_THREADS", "1")
+    import ctypes as C
+    from oracle.bind import Reference
+    R = Reference()
+    L = R.lib
+    L.ref_leaves_mvp_timed.restype = C.c_int
+    L.ref_leaves_mvp_timed.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_int64, C.c_double,
+                                       C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
+                                       C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    z = np.load(args.leaves)
+    coords = np.ascontiguousarray(z["coords"], dtype=np.float64)
+    d, n = coords.shape
+    dense = np.ascontiguousarray(z["dense"], dtype=np.int64)
+    aca = np.ascontiguousarray(z["aca"], dtype=np.int64)
+    x = np.ascontiguousarray(z["x"], dtype=np.float64)
+    out = np.zeros(n)
+    tm, fl = C.c_double(), C.c_double()
+    R._check(L.ref_leaves_mvp_timed(coords.ctypes.data, n, d, int(z["kernel"]), 0.0, int(z["k"]), float(z["eta"]),
+                                    dense.shape[0], dense.ctypes.data, aca.shape[0], aca.ctypes.data, x.ctypes.data,
+                                    args.reps, out.ctypes.data, C.byref(tm), C.byref(fl)))
+    return {"flops_per_rep": fl.value, "reps": args.reps, "t_mvp_ms": tm.value, "t_aca_ms": 0.0, "t_setup_ms": 0.0,
+            "rows": int(np.unique(np.concatenate([dense[:, 0], aca[:, 0]])).size) if dense.size + aca.size else 0,
+            "leaves": int(dense.shape[0] + aca.shape[0]), "threads": int(L.ref_threads())}
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--leaves", type=str, default="")
     ap.add_argument("--n", type=int, default=1 << 20)
     ap.add_argument("--d", type=int, default=2)
     ap.add_argument("--c-leaf", dest="c_leaf", type=int, default=64)
@@ -89,7 +119,8 @@ def main():
     ap.add_argument("--clusters", type=str, default="0")
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=0)
-    print(json.dumps(worker(ap.parse_args())))
+    args = ap.parse_args()
+    print(json.dumps(leaves_worker(args) if args.leaves else worker(args)))
 
 
 if __name__ == "__main__":

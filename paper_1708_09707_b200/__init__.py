@@ -76,7 +76,7 @@ class _Stats(C.Structure):
                 ("sum_n_adm", _d), ("S_lm", _d), ("S_ln", _d), ("S_d_own", _d), ("aca_rejections", _i64), ("dmax_leaf", _i32), ("row_begin", _i64),
                 ("row_end", _i64), ("device_bytes", _d),
                 ("S_d_stored", _d), ("near_sym", _i32), ("n_aca_batches", _i64), ("n_aca_chunks", _i64),
-                ("aca_rejected_entries", _i64), ("S_chain", _d)]
+                ("aca_rejected_entries", _i64), ("S_chain", _d), ("near_pairs", _i64), ("near_sym_rc", _i32)]
 
 
 def _sig(name, res, args):

@@ -152,6 +152,30 @@ struct AcaJob {
   const long long* dense_off;
 };
 
+// u_hat[i] / pivot (aca.cpp:466-470), correctly rounded: the pivot's correctly rounded
+// reciprocal y and one Markstein correction, q = a*y, r = fma(-q, p, a) (exact),
+// q' = fma(r, y, q) -- the IEEE quotient for operands in [2^-500, 2^500] (checked bit for
+// bit by tests/cpp/div_const_check.c); zeros (sign) and out-of-range operands take the
+// IEEE division.  One reciprocal per rank instead of m full divisions.
+struct PivotDiv {
+  double p, y;
+  bool fast;
+  __device__ __forceinline__ explicit PivotDiv(double pv) : p(pv) {
+    const double ap = fabs(pv);
+    fast = ap >= 0x1p-500 && ap <= 0x1p500;
+    y = fast ? __drcp_rn(pv) : 0.0;
+  }
+  __device__ __forceinline__ double operator()(double a) const {
+    const double aa = fabs(a);
+    if (fast && aa >= 0x1p-500 && aa <= 0x1p500) {
+      const double q = __dmul_rn(a, y);
+      const double r = __fma_rn(-q, p, a);
+      return __fma_rn(r, y, q);
+    }
+    return __ddiv_rn(a, p);
+  }
+};
+
 __device__ __forceinline__ void argmax_combine(double& bv, int& bi, double ov, int oi) {
   if (ov > bv || (ov == bv && oi < bi)) {
     bv = ov;
@@ -332,7 +356,8 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaJob J, KernelEntry<
       const double pivot_val = cbv(p);
       for (int l = tid; l < r; l += kAcaThreads) s_upiv[l] = U[uix(l, p)];
       __syncthreads();
-      for (int i = tid; i < m; i += kAcaThreads) U[uix(r, i)] = __ddiv_rn(cbv(i), pivot_val);
+      const PivotDiv pdiv(pivot_val);
+      for (int i = tid; i < m; i += kAcaThreads) U[uix(r, i)] = pdiv(cbv(i));
       {
         double yp[DIM > 0 ? DIM : 20];
         if constexpr (!DENSE) E.load(rl + p, yp);
@@ -707,11 +732,11 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
       }
       team_sync<NW>(team);
       if (r == 0) scale = s_misc[1];
-      const double pivot_val = acol[p];
+      const PivotDiv pdiv(acol[p]);
       // u_r = u_hat / pivot (aca.cpp:466-470), appended right-aligned
 #pragma unroll
       for (int q = 0; q < RPL; ++q) {
-        const double nu = rv[q] ? __ddiv_rn(acol[t + q * TT], pivot_val) : 0.0;
+        const double nu = rv[q] ? pdiv(acol[t + q * TT]) : 0.0;
 #pragma unroll
         for (int j = 0; j + 1 < KC; ++j) uR[q][j] = uR[q][j + 1];
         uR[q][KC - 1] = nu;
@@ -1004,8 +1029,8 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
       }
       __syncthreads();
       if (r == 0) scale = s_misc[1];
-      const double pivot_val = acol[p];
-      for (int i = t; i < m; i += TT) U[uix(r, i)] = __ddiv_rn(acol[i], pivot_val);
+      const PivotDiv pdiv(acol[p]);
+      for (int i = t; i < m; i += TT) U[uix(r, i)] = pdiv(acol[i]);
       ev_row += n;
       {
         double yp[YD];
@@ -1371,10 +1396,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
         if (t == 0) s_misc[3] = *rem(s_misc + 3, po);
       }
       __syncthreads();
-      const double pivot_val = s_misc[3];
+      const PivotDiv pdiv(s_misc[3]);
 #pragma unroll
       for (int q = 0; q < RPL; ++q) {
-        const double nu = rv[q] ? __ddiv_rn(acol[t + q * TT], pivot_val) : 0.0;
+        const double nu = rv[q] ? pdiv(acol[t + q * TT]) : 0.0;
 #pragma unroll
         for (int j = 0; j + 1 < KC; ++j) uR[q][j] = uR[q][j + 1];
         uR[q][KC - 1] = nu;

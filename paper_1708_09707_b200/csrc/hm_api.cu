@@ -171,10 +171,11 @@ hm_handle* new_handle(const hm_config* cfg, long long n, int d, int kernel, doub
 // caller streams are serialised on the device, not just on the host mutex.
 template <class F>
 void on_handle_stream(HMatrix& h, cudaStream_t caller, F&& f) {
-  if (caller == nullptr || caller == h.stream) {
+  if (caller == h.stream) {
     f(h.stream);
     return;
   }
+  if (caller == nullptr) caller = cudaStreamLegacy;  // CUDA convention: 0 = the legacy default stream
   HM_CUDA(cudaEventRecord(h.ev_join, caller));
   HM_CUDA(cudaStreamWaitEvent(h.stream, h.ev_join, 0));
   f(h.stream);
@@ -887,6 +888,8 @@ hm_status hm_get_stats(hm_handle* H, hm_stats* st) {
     st->aca_rejections = static_cast<int64_t>(rej[0]);
     st->aca_rejected_entries = static_cast<int64_t>(rej[1]);
     st->S_chain = h.S_chain;
+    st->near_pairs = h.n_pairs;
+    st->near_sym_rc = h.near_sym_rc ? 1 : 0;
     st->dmax_leaf = h.dmax_leaf;
     st->row_begin = h.row_begin;
     st->row_end = h.row_end;
@@ -994,9 +997,12 @@ hm_status hm_get_aca(hm_handle* H, int64_t* k_eff, int64_t* row_piv, int64_t* co
       HM_CUDA(cudaMemcpyAsync(hcp.data(), h.col_piv.get(), sizeof(int) * cnt * kmax, cudaMemcpyDeviceToHost, s));
     }
     HM_CUDA(cudaStreamSynchronize(s));
+    long long ou = 0, ov = 0;  // output offsets: k x m and k x n per leaf, rank-major
     for (long long b = 0; b < cnt; ++b) {
       k_eff[b] = hk[b];
       const long long m = h.aca.h_m[b], n = h.aca.h_n[b];
+      // device layout: stride kmax, or ke2 = k_eff rounded to even (compacted stored factors)
+      const long long ks = h.compact ? ((hk[b] + 1) & ~1) : kmax;
       for (long long l = 0; l < kmax; ++l) {
         row_piv[b * kmax + l] = hrp[b * kmax + l];
         col_piv[b * kmax + l] = hcp[b * kmax + l];
@@ -1004,13 +1010,14 @@ hm_status hm_get_aca(hm_handle* H, int64_t* k_eff, int64_t* row_piv, int64_t* co
         const int sh = h.u_tile_shift;
         if (u)
           for (long long i = 0; i < m; ++i) {
-            const long long src =
-                sh < 0 ? l * m + i : ((((i >> sh) * kmax) + l) << sh) + (i & ((1ll << sh) - 1));
-            u[uo[b] + l * m + i] = live ? hu[uo[b] + src] : 0.0;
+            const long long src = sh < 0 ? l * m + i : ((((i >> sh) * ks) + l) << sh) + (i & ((1ll << sh) - 1));
+            u[ou + l * m + i] = live ? hu[uo[b] + src] : 0.0;
           }
         if (v)
-          for (long long j = 0; j < n; ++j) v[vo[b] + l * n + j] = live ? hv[vo[b] + j * kmax + l] : 0.0;
+          for (long long j = 0; j < n; ++j) v[ov + l * n + j] = live ? hv[vo[b] + j * ks + l] : 0.0;
       }
+      ou += kmax * m;
+      ov += kmax * n;
     }
   });
 }

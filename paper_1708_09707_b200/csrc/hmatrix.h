@@ -128,6 +128,7 @@ struct HMatrix : HandleStreams {
   int u_tile_shift = -1;
   bool tma_rows = false;
   bool tma_far = false;  // recompute mode: far-field chunks on the TMA row kernel (U row-tiled)
+  bool compact = false;  // stored factors with stride ke2 = k_eff rounded to even (mvp.cu compact_factors)
   DevBuf<int> k_eff, row_piv, col_piv;
   // host copies of the factor offsets (fixed at setup: the product never reads them back)
   std::vector<long long> h_uoff, h_voff;

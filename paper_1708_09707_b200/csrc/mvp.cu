@@ -143,6 +143,7 @@ struct RowArgs {
   const double* U;
   const double* t;
   int kmax;
+  int compact = 0;               // factors stored with stride ke2 = k_eff rounded up to even
   long long a_lo, a_hi;
   // canonical leaf spans per deepest row cluster
   const int* row_cluster;
@@ -607,7 +608,8 @@ __global__ void __launch_bounds__(S) rows_tma_kernel(TmaArgs A) {
                      : "memory");
       } else {
         mbar_expect_tx(&bars[st], static_cast<unsigned>(ke2) * (S + 1) * 8u);
-        bulk_g2s_hint(sdata[st], a.U + (__ldg(a.a_uoff + L) - a.a_ubase) + q * a.kmax * S,
+        // U row tiles [i/S][l][i%S]: tile stride kmax*S, or ke2*S when compacted
+        bulk_g2s_hint(sdata[st], a.U + (__ldg(a.a_uoff + L) - a.a_ubase) + q * (a.compact ? ke2 : a.kmax) * S,
                       static_cast<unsigned>(ke2) * S * 8u, &bars[st], pol_stream);
         bulk_g2s_hint(saux[st], a.t + static_cast<long long>(L) * a.kmax, static_cast<unsigned>(ke2) * 8u, &bars[st],
                       pol_keep);
@@ -735,6 +737,7 @@ RowArgs base_row_args(HMatrix& h) {
   a.U = h.U.get();
   a.t = h.t.get();
   a.kmax = static_cast<int>(h.cfg.k);
+  a.compact = h.compact ? 1 : 0;
   a.row_cluster = h.row_cluster.get();
   a.dspan_ptr = h.dspan_ptr.get();
   a.dspans = h.dspans.get();
@@ -899,8 +902,8 @@ __global__ void __launch_bounds__(WARPS * 32) t_pair_kernel(const int* __restric
                                                             const long long* __restrict__ v_off, long long v_base,
                                                             const double* __restrict__ V,
                                                             const double* __restrict__ xm, int* __restrict__ counter,
-                                                            double* __restrict__ t) {
-  constexpr int KM = 16;
+                                                            double* __restrict__ t, int compact) {
+  constexpr int KM = 16;  // kmax; V rows are KM doubles apart, or ke2 = k_eff rounded to even (compact)
   constexpr int SV = CH * KM;      // doubles of one leaf's V chunk
   constexpr int SX = CH + 2;       // doubles of one leaf's x chunk
   constexpr int STAGE = 2 * SV + 2 * SX;
@@ -959,7 +962,9 @@ __global__ void __launch_bounds__(WARPS * 32) t_pair_kernel(const int* __restric
     unsigned bytes = 0;
     int xoff[2] = {0, 0};
     const int nl = pair ? 2 : 1;
-    for (int q = 0; q < nl; ++q) bytes += pke[q] > 0 ? static_cast<unsigned>(cnt) * KM * 8u : 0u;
+    int vs[2];
+    for (int q = 0; q < 2; ++q) vs[q] = compact ? ((pke[q] + 1) & ~1) : KM;
+    for (int q = 0; q < nl; ++q) bytes += pke[q] > 0 ? static_cast<unsigned>(cnt) * vs[q] * 8u : 0u;
     // leaves of a pair with the same column cluster (the queue is column-ordered within
     // a size) share one x segment
     const bool xshare = pair && pke[0] > 0 && pke[1] > 0 && pcl[0] == pcl[1];
@@ -985,8 +990,8 @@ __global__ void __launch_bounds__(WARPS * 32) t_pair_kernel(const int* __restric
       mbar_expect_tx(&bars[st], bytes);
       for (int q = 0; q < nl; ++q) {
         if (pke[q] == 0) continue;
-        bulk_g2s_hint(dv + q * SV, V + pvo[q] + static_cast<long long>(pj) * KM, static_cast<unsigned>(cnt) * KM * 8u,
-                      &bars[st], pol_stream);
+        bulk_g2s_hint(dv + q * SV, V + pvo[q] + static_cast<long long>(pj) * vs[q],
+                      static_cast<unsigned>(cnt) * vs[q] * 8u, &bars[st], pol_stream);
         if (q == 1 && xshare) continue;
         const long long xa = (pcl[q] + pj) & ~1ll;
         bulk_g2s_hint(dv + 2 * SV + q * SX, xm + xa, static_cast<unsigned>((xoff[q] + cnt + 1) & ~1) * 8u, &bars[st],
@@ -1023,6 +1028,7 @@ __global__ void __launch_bounds__(WARPS * 32) t_pair_kernel(const int* __restric
     const int b = half ? d[1] : b0;
     const int cnt = d[2], flags = d[5];
     const int ke = half ? d[7] : d[6];
+    const int vst = compact ? ((ke + 1) & ~1) : KM;  // row stride of this half's V chunk
     const double* dv = sv + static_cast<long long>(st) * STAGE + half * SV + l;
     const int xh = (flags & 4) ? 0 : half;  // shared x segment: both halves read slot 0
     const double* dx = sv + static_cast<long long>(st) * STAGE + 2 * SV + xh * SX + (half ? d[4] : d[3]);
@@ -1036,13 +1042,13 @@ __global__ void __launch_bounds__(WARPS * 32) t_pair_kernel(const int* __restric
         double vv[16], xx[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
-          vv[u] = dv[(q + u) * KM];
+          vv[u] = dv[(q + u) * vst];
           xx[u] = dx[q + u];
         }
 #pragma unroll
         for (int u = 0; u < 16; ++u) acc = hadd(acc, hmul(vv[u], xx[u]));
       }
-      for (; q < cnt; ++q) acc = hadd(acc, hmul(dv[q * KM], dx[q]));
+      for (; q < cnt; ++q) acc = hadd(acc, hmul(dv[q * vst], dx[q]));
     }
     if ((flags & 2) && b >= 0) t[static_cast<long long>(b) * KM + l] = l < ke ? acc : 0.0;
     __syncwarp();
@@ -1068,7 +1074,8 @@ void launch_pair(HMatrix& h, const int* order, long long njobs, long long v_base
   HM_CUDA(cudaMemsetAsync(h.counter.get(), 0, sizeof(int), s));
   t_pair_kernel<CH, NST, WARPS><<<grid, WARPS * 32, smem, s>>>(order, njobs, h.aca.cl.get(),
                                                               h.aca.n.get(), h.k_eff.get(), h.v_off.get(), v_base,
-                                                              h.V.get(), h.xm.get(), h.counter.get(), h.t.get());
+                                                              h.V.get(), h.xm.get(), h.counter.get(), h.t.get(),
+                                                              h.compact ? 1 : 0);
   HM_LAUNCH_CHECK();
 }
 
@@ -1284,6 +1291,93 @@ void launch_near_pairs(HMatrix& h, cudaStream_t s) {
   HM_LAUNCH_CHECK();
 }
 
+// Compacted stored factors (regular geometry, k = 16): per admissible leaf, V rows
+// (n x k interleaved) and the U row tiles ([i/S][l][i%S]) keep only ke2 = k_eff rounded up
+// to even ranks, like the reference's l < k_eff loops (aca.cpp:610-617) -- the product
+// streams exactly the ranks it folds.
+__global__ void compact_v_kernel(const int* __restrict__ nn, const int* __restrict__ k_eff, long long lo,
+                                 long long cnt, const long long* __restrict__ vo_old, long long vb_old,
+                                 const long long* __restrict__ vo_new, int kmax, const double* __restrict__ V,
+                                 double* __restrict__ V2) {
+  for (long long q = blockIdx.x; q < cnt; q += gridDim.x) {
+    const long long b = lo + q;
+    const int n = nn[b], ke2 = (k_eff[b] + 1) & ~1;
+    const double* src = V + (vo_old[b] - vb_old);
+    double* dst = V2 + vo_new[q];
+    for (long long e = threadIdx.x; e < static_cast<long long>(n) * ke2; e += blockDim.x) {
+      const long long j = e / ke2, l = e - j * ke2;
+      dst[e] = src[j * kmax + l];
+    }
+  }
+}
+__global__ void compact_u_kernel(const int* __restrict__ mm, const int* __restrict__ k_eff, long long lo,
+                                 long long cnt, const long long* __restrict__ uo_old, long long ub_old,
+                                 const long long* __restrict__ uo_new, int kmax, int S, const double* __restrict__ U,
+                                 double* __restrict__ U2) {
+  for (long long q = blockIdx.x; q < cnt; q += gridDim.x) {
+    const long long b = lo + q;
+    const int m = mm[b], ke2 = (k_eff[b] + 1) & ~1;
+    const double* src = U + (uo_old[b] - ub_old);
+    double* dst = U2 + uo_new[q];
+    const long long tile = static_cast<long long>(ke2) * S;
+    for (long long e = threadIdx.x; e < static_cast<long long>(m) * ke2; e += blockDim.x) {
+      const long long tq = e / tile, w = e - tq * tile;  // w = l * S + i%S
+      dst[e] = src[tq * kmax * S + w];
+    }
+  }
+}
+
+static void compact_factors(HMatrix& h, const int* ke, long long lo, long long hi, cudaStream_t s) {
+  const long long cnt = hi - lo, kmax = h.cfg.k, S = h.n >> h.dmax_leaf;
+  if (cnt <= 0) return;
+  std::vector<long long> uo(cnt + 1, 0), vo(cnt + 1, 0);
+  for (long long q = 0; q < cnt; ++q) {
+    const long long ke2 = (ke[q] + 1) & ~1;
+    uo[q + 1] = uo[q] + ke2 * h.aca.h_m[lo + q];
+    vo[q + 1] = vo[q] + ke2 * h.aca.h_n[lo + q];
+  }
+  DevBuf<long long> duo, dvo;
+  duo.alloc(cnt + 1, s);
+  dvo.alloc(cnt + 1, s);
+  HM_CUDA(cudaMemcpyAsync(duo.get(), uo.data(), sizeof(long long) * (cnt + 1), cudaMemcpyHostToDevice, s));
+  HM_CUDA(cudaMemcpyAsync(dvo.get(), vo.data(), sizeof(long long) * (cnt + 1), cudaMemcpyHostToDevice, s));
+  const unsigned grid = static_cast<unsigned>(std::min<long long>(cnt, 148ll * 64));
+  const long long ub = h.h_uoff[lo], vb = h.h_voff[lo];
+  {  // V, then U: one old and one new buffer live at a time
+    DevBuf<double> V2;
+    V2.alloc(std::max(vo[cnt], 1ll), s);
+    compact_v_kernel<<<grid, 256, 0, s>>>(h.aca.n.get(), h.k_eff.get(), lo, cnt, h.v_off.get(), vb, dvo.get(),
+                                          static_cast<int>(kmax), h.V.get(), V2.get());
+    HM_LAUNCH_CHECK();
+    HM_CUDA(cudaStreamSynchronize(s));
+    h.V = std::move(V2);
+  }
+  {
+    DevBuf<double> U2;
+    U2.alloc(std::max(uo[cnt], 1ll), s);
+    compact_u_kernel<<<grid, 256, 0, s>>>(h.aca.m.get(), h.k_eff.get(), lo, cnt, h.u_off.get(), ub, duo.get(),
+                                          static_cast<int>(kmax), static_cast<int>(S), h.U.get(), U2.get());
+    HM_LAUNCH_CHECK();
+    HM_CUDA(cudaStreamSynchronize(s));
+    h.U = std::move(U2);
+  }
+  // new offsets (relative to the own range; the chunk bases become 0)
+  for (long long q = 0; q <= cnt; ++q) {
+    h.h_uoff[lo + q] = uo[q];
+    h.h_voff[lo + q] = vo[q];
+  }
+  HM_CUDA(cudaMemcpyAsync(h.u_off.get() + lo, uo.data(), sizeof(long long) * (cnt + 1), cudaMemcpyHostToDevice, s));
+  HM_CUDA(cudaMemcpyAsync(h.v_off.get() + lo, vo.data(), sizeof(long long) * (cnt + 1), cudaMemcpyHostToDevice, s));
+  for (AcaChunk& c : h.chunks) {
+    c.ub = h.h_uoff[c.c0];
+    c.vb = h.h_voff[c.c0];
+    c.ue = h.h_uoff[c.c1];
+    c.ve = h.h_voff[c.c1];
+  }
+  HM_CUDA(cudaStreamSynchronize(s));
+  h.compact = true;
+}
+
 // S_l = S_lm + S_ln and the chain work S_chain of the own leaves [lo, hi) from k_eff
 void rank_sums(HMatrix& h, const int* ke, long long lo, long long hi) {
   h.S_l = h.S_lm = h.S_ln = h.S_chain = 0;
@@ -1317,6 +1411,8 @@ void plan_far_field(HMatrix& h, cudaStream_t s) {
   h.row_piv.alloc(std::max(h.aca.count * kmax, 1ll), s);
   h.col_piv.alloc(std::max(h.aca.count * kmax, 1ll), s);
   h.t.alloc(std::max(h.aca.count * kmax, 1ll), s);
+  h.counter.alloc(1, s);  // job counter of the V^T x fold kernels
+  h.counter.zero(s);
   reset_aca_rejections(h, s);
   long long lo, hi;
   own_range(h.aca, h.row_begin, h.row_end, lo, hi);
@@ -1410,6 +1506,7 @@ void plan_far_field(HMatrix& h, cudaStream_t s) {
     HM_CUDA(cudaStreamSynchronize(s));
     h.keff_known = true;
     rank_sums(h, ke.data(), lo, hi);
+    if (h.tma_rows && kmax == 16 && std::getenv("HM_NO_COMPACT") == nullptr) compact_factors(h, ke.data(), lo, hi, s);
   }
 }
 

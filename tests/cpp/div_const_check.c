@@ -43,6 +43,25 @@ int main(int argc, char** argv) {
       }
     }
   }
+  /* general divisors (the ACA pivot, aca.cpp:466-470): y = RN(1/p), both operands in
+   * [2^-500, 2^500] as the device fast path requires */
+  for (long long t = 0; t < 64 * samples; ++t) {
+    const uint64_t ea = 1023 - 60 + (next_u64() % 64), ep = 1023 - 60 + (next_u64() % 64);
+    uint64_t ma = next_u64() & ((1ull << 52) - 1), mp = next_u64() & ((1ull << 52) - 1);
+    if ((t & 1023) < 8) mp = (1ull << 52) - 1 - (uint64_t)(t & 7);  /* significand of p all ones */
+    const double a = from_bits((ea << 52) | ma) * ((t & 2) ? -1.0 : 1.0);
+    const double p = from_bits((ep << 52) | mp) * ((t & 4) ? -1.0 : 1.0);
+    const double y = 1.0 / p;
+    const double q = a * y;
+    const double r = fma(-q, p, a);
+    const double q1 = fma(r, y, q);
+    const double want = a / p;
+    ++total;
+    if (memcmp(&q1, &want, 8) != 0) {
+      if (bad < 5) printf("mismatch (general) a=%a p=%a got %a want %a\n", a, p, q1, want);
+      ++bad;
+    }
+  }
   printf("{\"checked\": %lld, \"mismatches\": %lld}\n", total, bad);
   return bad ? 1 : 0;
 }

@@ -1,3 +1,4 @@
+import os
 """Live cross-check of the C restatement against the unmodified reference (oracle/_ref),
 on randomised configurations, plus the SURVEY.md findings the parity targets rest on.
 Skipped where oracle/_ref is not built."""
@@ -120,3 +121,40 @@ def test_reference_leaf_csv_is_the_merged_canonical_list(oracle, reference, cfg,
     order = np.lexsort((rows[:, 3], rows[:, 2], rows[:, 1], rows[:, 0]))
     want = np.column_stack([rows[order], flags[order]])
     assert np.array_equal(got, want)
+
+
+def test_reference_leaf_sample_driver_equals_reference_mvp(reference, tmp_path):
+    """The recompute-mode CPU baseline (ref_leaves_mvp_timed, bench.py) runs the
+    reference's own mvp() body over an explicit leaf list: with every leaf of a reference
+    setup it reproduces the reference's product bitwise (Morton order)."""
+    import subprocess
+    import sys
+    from paper_1708_09707_b200.inputs import symmetric, uniform_points
+    n, d = 3000, 3
+    P = uniform_points(n, d, 42)
+    h = reference.setup(P, kernel=1, c_leaf=48, k=12)
+    coords, perm = h.points()
+    x = symmetric(5, n)
+    z = h.mvp(x)
+    f = tmp_path / "leaves.npz"
+    np.savez(f, coords=coords, dense=h.leaves(0, boxes=False).rows, aca=h.leaves(1, boxes=False).rows,
+             x=x[perm], kernel=1, k=12, eta=1.5)
+    import ctypes as C
+    L = reference.lib
+    L.ref_leaves_mvp_timed.restype = C.c_int
+    L.ref_leaves_mvp_timed.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_int64, C.c_double,
+                                       C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
+                                       C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    dense = np.ascontiguousarray(h.leaves(0, boxes=False).rows, dtype=np.int64)
+    aca = np.ascontiguousarray(h.leaves(1, boxes=False).rows, dtype=np.int64)
+    xm = np.ascontiguousarray(x[perm])
+    zm = np.zeros(n)
+    tm, fl = C.c_double(), C.c_double()
+    assert L.ref_leaves_mvp_timed(coords.ctypes.data, n, d, 1, 0.0, 12, 1.5, dense.shape[0], dense.ctypes.data,
+                                  aca.shape[0], aca.ctypes.data, xm.ctypes.data, 1, zm.ctypes.data, C.byref(tm),
+                                  C.byref(fl)) == 0
+    assert np.array_equal(zm.view(np.uint64), z[perm].view(np.uint64))
+    out = subprocess.run([sys.executable, "-m", "oracle.refbench", "--leaves", str(f), "--reps", "1"],
+                         capture_output=True, text=True,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0, out.stderr
