@@ -122,6 +122,41 @@ struct KernelEntry {
     }
     return phi_kind<KIND>(kp, r2);
   }
+  __device__ __forceinline__ double r2_of(const double* y, long long j) const {
+    double r2 = 0.0;
+    if constexpr (DIM > 0) {
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        const double dx = hsub(y[a], __ldg(coords + a * n + j));
+        r2 = hadd(r2, hmul(dx, dx));
+      }
+    } else {
+      for (int a = 0; a < d; ++a) {
+        const double dx = hsub(y[a], __ldg(coords + a * n + j));
+        r2 = hadd(r2, hmul(dx, dx));
+      }
+    }
+    return r2;
+  }
+  // two entries with overlapped dependency chains (kernel_math.cuh phi_x2), bitwise equal
+  // to two eval() calls: rows y0, y1 against point j, or row y against points j0, j1
+  __device__ __forceinline__ void eval2(const double* y0, const double* y1, long long j, double& a0,
+                                        double& a1) const {
+    if constexpr (KIND >= 0) {
+      phi_x2<KIND>(kp, r2_of(y0, j), r2_of(y1, j), a0, a1);
+    } else {
+      a0 = eval(y0, j);
+      a1 = eval(y1, j);
+    }
+  }
+  __device__ __forceinline__ void eval2c(const double* y, long long j0, long long j1, double& a0, double& a1) const {
+    if constexpr (KIND >= 0) {
+      phi_x2<KIND>(kp, r2_of(y, j0), r2_of(y, j1), a0, a1);
+    } else {
+      a0 = eval(y, j0);
+      a1 = eval(y, j1);
+    }
+  }
 };
 
 struct AcaJob {
@@ -157,6 +192,8 @@ struct AcaJob {
 // q' = fma(r, y, q) -- the IEEE quotient for operands in [2^-500, 2^500] (checked bit for
 // bit by tests/cpp/div_const_check.c); zeros (sign) and out-of-range operands take the
 // IEEE division.  One reciprocal per rank instead of m full divisions.
+static __device__ __noinline__ double ieee_div_slow(double a, double p) { return __ddiv_rn(a, p); }
+
 struct PivotDiv {
   double p, y;
   bool fast;
@@ -172,7 +209,7 @@ struct PivotDiv {
       const double r = __fma_rn(-q, p, a);
       return __fma_rn(r, y, q);
     }
-    return __ddiv_rn(a, p);
+    return ieee_div_slow(a, p);  // out of line: keeps the hot loops' register footprint
   }
 };
 
@@ -549,8 +586,13 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
             vb = V + static_cast<long long>(col) * kmax + (r - KC);
             vs = 1;
           }
-          double a0 = rv[0] ? entry(0, cl + col) : 0.0;
-          double a1 = rv[1] ? entry(1, cl + col) : 0.0;
+          double a0, a1;
+          if constexpr (DIM > 0) {
+            E.eval2(y[0], y[1], cl + col, a0, a1);  // invalid rows: finite dummies, never stored
+          } else {
+            a0 = rv[0] ? entry(0, cl + col) : 0.0;
+            a1 = rv[1] ? entry(1, cl + col) : 0.0;
+          }
           Chain<KC>::run2(a0, a1, uR[0], uR[1], r, vb, vs);
           if (rv[0]) dst[t] = a0;
           if (rv[1]) dst[t + TT] = a1;
@@ -749,23 +791,28 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
         double uP[KC];  // u_l[p], right-aligned (aca_chain.cuh)
 #pragma unroll
         for (int j = 0; j < KC; ++j) uP[j] = j >= KC - r ? s_up[j - (KC - r)] : 0.0;
-        for (int j = t; j < n; j += TT) {
-          double a;
-          if (j >= next && j < next + filled) {
-            a = s_win[(j % W) * PS + p];
+        // two columns per step (j, j + TT): their entry evaluations and chains overlap
+        auto vbase = [&](int j) -> const double* {
+          if constexpr (VSM) return s_v + static_cast<long long>(r - KC) * NCAP + j;
+          else return V + static_cast<long long>(j) * kmax + (r - KC);
+        };
+        constexpr int VS = VSM ? NCAP : 1;
+        for (int j = t; j < n; j += 2 * TT) {
+          const int j1 = j + TT;
+          const bool in0 = j >= next && j < next + filled;
+          const bool ok1 = j1 < n, in1 = ok1 && j1 >= next && j1 < next + filled;
+          double a0, a1;
+          if (in0 && (in1 || !ok1)) {
+            a0 = s_win[(j % W) * PS + p];
+            a1 = ok1 ? s_win[(j1 % W) * PS + p] : 0.0;
           } else {
-            const double* vb;
-            int vs;
-            if constexpr (VSM) {
-              vb = s_v + static_cast<long long>(r - KC) * NCAP + j;
-              vs = NCAP;
-            } else {
-              vb = V + static_cast<long long>(j) * kmax + (r - KC);
-              vs = 1;
-            }
-            a = Chain<KC>::run(E.eval(yp, cl + j), uP, r, vb, vs);
+            E.eval2c(yp, cl + j, cl + (ok1 ? j1 : j), a0, a1);
+            Chain<KC>::run2v(a0, a1, uP, r, vbase(j), vbase(ok1 ? j1 : j), VS);
+            if (in0) a0 = s_win[(j % W) * PS + p];
+            if (in1) a1 = s_win[(j1 % W) * PS + p];
           }
-          vat(r, j) = a;
+          vat(r, j) = a0;
+          if (ok1) vat(r, j1) = a1;
         }
       }
       team_sync<NW>(team);
@@ -924,8 +971,9 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
           E.load(rl + (ok1 ? i1 : i0), y1);
           for (int co = filled; co < wcols; ++co) {
             const int col = next + co;
-            double a0 = E.eval(y0, cl + col);
-            double a1 = ok1 ? E.eval(y1, cl + col) : 0.0;
+            double a0, a1;
+            E.eval2(y0, y1, cl + col, a0, a1);
+            if (!ok1) a1 = 0.0;
             Chain<KC>::run2(a0, a1, uR[0], uR[1], r, V + static_cast<long long>(col) * kmax + (r - KC), 1);
             double* dst = win + static_cast<long long>(col % W) * PS;
             dst[i0] = a0;
@@ -1038,14 +1086,24 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
         double uP[KC];  // u_l[p], right-aligned: every V-row load of the chain issues up front
 #pragma unroll
         for (int j = 0; j < KC; ++j) uP[j] = j >= KC - r ? s_up[j - (KC - r)] : 0.0;
-        for (int j = t; j < n; j += TT) {
-          double a;
-          if (j >= next && j < next + filled) {
-            a = win[static_cast<long long>(j % W) * PS + p];
+        for (int j = t; j < n; j += 2 * TT) {
+          const int j1 = j + TT;
+          const bool ok1 = j1 < n;
+          const int jj = ok1 ? j1 : j;
+          const bool in0 = j >= next && j < next + filled, in1 = jj >= next && jj < next + filled;
+          double a0, a1;
+          if (in0 && in1) {
+            a0 = win[static_cast<long long>(j % W) * PS + p];
+            a1 = win[static_cast<long long>(jj % W) * PS + p];
           } else {
-            a = Chain<KC>::run(E.eval(yp, cl + j), uP, r, V + static_cast<long long>(j) * kmax + (r - KC), 1);
+            E.eval2c(yp, cl + j, cl + jj, a0, a1);
+            Chain<KC>::run2v(a0, a1, uP, r, V + static_cast<long long>(j) * kmax + (r - KC),
+                             V + static_cast<long long>(jj) * kmax + (r - KC), 1);
+            if (in0) a0 = win[static_cast<long long>(j % W) * PS + p];
+            if (in1) a1 = win[static_cast<long long>(jj % W) * PS + p];
           }
-          V[static_cast<long long>(j) * kmax + r] = a;
+          V[static_cast<long long>(j) * kmax + r] = a0;
+          if (ok1) V[static_cast<long long>(j1) * kmax + r] = a1;
         }
       }
       __syncthreads();
@@ -1201,8 +1259,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
         for (int co = filled; co < wcols; ++co) {
           const int col = next + co;
           double* dst = s_win + (col % W) * PS;
-          double a0 = rv[0] ? entry(0, cl + col) : 0.0;
-          double a1 = rv[1] ? entry(1, cl + col) : 0.0;
+          double a0, a1;
+          if constexpr (DIM > 0) {
+            E.eval2(y[0], y[1], cl + col, a0, a1);
+          } else {
+            a0 = rv[0] ? entry(0, cl + col) : 0.0;
+            a1 = rv[1] ? entry(1, cl + col) : 0.0;
+          }
           Chain<KC>::run2(a0, a1, uR[0], uR[1], r, V + static_cast<long long>(col) * kmax + (r - KC), 1);
           if (rv[0]) dst[t] = a0;
           if (rv[1]) dst[t + TT] = a1;
@@ -1412,9 +1475,17 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
         double uP[KC];
 #pragma unroll
         for (int j = 0; j < KC; ++j) uP[j] = j >= KC - r ? s_up[j - (KC - r)] : 0.0;
-        for (int j = cr * TT + t; j < n; j += CL * TT)
-          V[static_cast<long long>(j) * kmax + r] =
-              Chain<KC>::run(E.eval(yp, cl + j), uP, r, V + static_cast<long long>(j) * kmax + (r - KC), 1);
+        for (int j = cr * TT + t; j < n; j += 2 * CL * TT) {
+          const int j1 = j + CL * TT;
+          const bool ok1 = j1 < n;
+          const int jj = ok1 ? j1 : j;
+          double a0, a1;
+          E.eval2c(yp, cl + j, cl + jj, a0, a1);
+          Chain<KC>::run2v(a0, a1, uP, r, V + static_cast<long long>(j) * kmax + (r - KC),
+                           V + static_cast<long long>(jj) * kmax + (r - KC), 1);
+          V[static_cast<long long>(j) * kmax + r] = a0;
+          if (ok1) V[static_cast<long long>(j1) * kmax + r] = a1;
+        }
       }
       cluster.sync();  // v_r visible to the whole cluster (release / acquire)
       if (cr == po && t == pt) s_used[pl] = 1;

@@ -8,6 +8,9 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <thread>
+#include <atomic>
+#include <type_traits>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -162,6 +165,47 @@ hm_handle* new_handle(const hm_config* cfg, long long n, int d, int kernel, doub
   H->h.d = d;
   H->h.create(cfg ? cfg->device : 0);  // streams + events, released by ~HandleStreams
   return H.release();
+}
+
+// dst <- src (host memory) with up to 4 threads over 1 MB chunks; after each chunk is in
+// place, on_chunk(offset, length) is called from the calling thread in order (used to
+// queue the chunk's DMA while later chunks are still being copied).
+template <class F>
+void staged_copy(void* dst, const void* src, size_t bytes, F&& on_chunk) {
+  constexpr size_t kChunk = size_t(1) << 20;
+  const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+  auto copy = [&](size_t c) {
+    const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+    std::memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, len);
+  };
+  constexpr bool kNotify = !std::is_same<std::decay_t<F>, std::nullptr_t>::value;
+  if (nchunks <= 2) {
+    for (size_t c = 0; c < nchunks; ++c) {
+      copy(c);
+      if constexpr (kNotify) on_chunk(c * kChunk, std::min(kChunk, bytes - c * kChunk));
+    }
+    return;
+  }
+  const unsigned nthr = 4;
+  std::atomic<size_t> next{0};
+  std::vector<std::atomic<int>> done(nchunks);
+  for (auto& d : done) d.store(0, std::memory_order_relaxed);
+  auto worker = [&] {
+    for (size_t c; (c = next.fetch_add(1)) < nchunks;) {
+      copy(c);
+      done[c].store(1, std::memory_order_release);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (unsigned i = 1; i < nthr; ++i) pool.emplace_back(worker);
+  worker();
+  if constexpr (kNotify) {
+    for (size_t c = 0; c < nchunks; ++c) {
+      while (!done[c].load(std::memory_order_acquire)) std::this_thread::yield();
+      on_chunk(c * kChunk, std::min(kChunk, bytes - c * kChunk));
+    }
+  }
+  for (auto& th : pool) th.join();
 }
 
 // Runs f(stream) on the handle's stream, ordered after the work already queued on
@@ -471,8 +515,12 @@ hm_status hm_mvp(hm_handle* H, const double* x, double* z, hm_timings* t) {
     // through a driver buffer at a fraction of it)
     if (!H->pin_x) HM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&H->pin_x), bytes));
     if (!H->pin_z) HM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&H->pin_z), bytes));
-    std::memcpy(H->pin_x, x, bytes);
-    HM_CUDA(cudaMemcpyAsync(h.xin.get(), H->pin_x, bytes, cudaMemcpyHostToDevice, s));
+    // x: host copies into the pinned staging run on a few threads, chunk by chunk, and each
+    // chunk's DMA is queued as soon as it is staged (copy and transfer overlap)
+    staged_copy(H->pin_x, x, bytes, [&](size_t off, size_t len) {
+      HM_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(h.xin.get()) + off, reinterpret_cast<char*>(H->pin_x) + off, len,
+                              cudaMemcpyHostToDevice, s));
+    });
     h.phase_events = true;
     try {
       product(H, h.xin.get(), h.zout.get(), s);
@@ -483,7 +531,7 @@ hm_status hm_mvp(hm_handle* H, const double* x, double* z, hm_timings* t) {
     h.phase_events = false;
     HM_CUDA(cudaMemcpyAsync(H->pin_z, h.zout.get(), bytes, cudaMemcpyDeviceToHost, s));
     HM_CUDA(cudaStreamSynchronize(s));
-    std::memcpy(z, H->pin_z, bytes);
+    staged_copy(z, H->pin_z, bytes, nullptr);
     h.tm.mvp_ms = ms_since(t0);
     // MvpTimings (hmatrix.cpp:117-121): dense (near-field) and ACA (far-field) phases
     float dms = 0.f, ams = 0.f;

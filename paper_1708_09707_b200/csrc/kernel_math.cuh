@@ -54,7 +54,7 @@ static __constant__ K1Tables kK1Dev =
     ;
 #endif
 
-#ifdef __CUDA_ARCH__
+#ifdef __CUDACC__
 __device__ __forceinline__ double div_by_const(double a, double den, double rden) {
   const double q = __dmul_rn(a, rden);
   const double r = __fma_rn(-q, den, a);
@@ -142,6 +142,133 @@ HM_HD double phi_r2(const KernelParams& kp, double r2) {
   const double r = hm_sqrt(r2);
   return hmul(hmul(bessel_k1(r), r), kp.matern_norm);
 }
+
+// ---------------------------------------------------------------------------------
+// Two independent entries at once (device).  Each value goes through exactly the
+// operations of the scalar function above (bitwise identical results); the two
+// instruction streams are merged so the FP64 dependency chains overlap: the main paths
+// are straight-line for both values, the rare special cases are fixed up afterwards,
+// and the K1 series runs both loops in one with per-value exit masks.
+#ifdef __CUDACC__
+// glibc exp main path (|x| in [2^-54, 512)); anything else takes glibc_exp afterwards
+__device__ __forceinline__ double exp_main(double x) {
+  const GlibcExpData& D = kExpDataDev;
+  double kd = hfma(x, D.invln2N, D.shift);
+  const unsigned long long ki = as_u64(kd);
+  kd = hsub(kd, D.shift);
+  double r = hfma(kd, D.negln2hiN, x);
+  r = hfma(kd, D.negln2loN, r);
+  const int idx = static_cast<int>(2u * (ki & 127u));
+  const unsigned long long top = ki << 45;
+  const double tail = as_double(exp_tab(idx));
+  const unsigned long long sbits = exp_tab(idx + 1) + top;
+  const double t1 = hfma(r, D.C3, D.C2);
+  const double s = hadd(r, tail);
+  const double r2 = hmul(r, r);
+  const double t2 = hfma(r, D.C5, D.C4);
+  const double p = hfma(t1, r2, s);
+  const double r4 = hmul(r2, r2);
+  const double tmp = hfma(r4, t2, p);
+  const double scale = as_double(sbits);
+  return hfma(scale, tmp, scale);
+}
+__device__ __forceinline__ bool exp_main_ok(double x) {
+  const unsigned abstop = static_cast<unsigned>(as_u64(x) >> 52) & 0x7ffu;
+  return abstop - 969u <= 62u;
+}
+__device__ __forceinline__ void glibc_exp_x2(double x0, double x1, double& e0, double& e1) {
+  e0 = exp_main(x0);
+  e1 = exp_main(x1);
+  if (!exp_main_ok(x0)) e0 = glibc_exp(x0);
+  if (!exp_main_ok(x1)) e1 = glibc_exp(x1);
+}
+
+// glibc log main path (not within [1 - 2^-4, 1 + 0x1.09p-4], positive normal)
+__device__ __forceinline__ double log_main(double x) {
+  const GlibcLogData& D = kLogDataDev;
+  const unsigned long long ix = as_u64(x);
+  const unsigned long long tmp = ix - 0x3fe6000000000000ull;
+  const int i = static_cast<int>((tmp >> 45) & 127u);
+  const int k = static_cast<int>(static_cast<long long>(tmp) >> 52);
+  const unsigned long long iz = ix - (tmp & (0xfffull << 52));
+  const double invc = log_tab(2 * i);
+  const double logc = log_tab(2 * i + 1);
+  const double z = as_double(iz);
+  const double kd = static_cast<double>(k);
+  const double w = hfma(kd, D.ln2hi, logc);
+  const double r = hfma(z, invc, -1.0);
+  const double p1 = hfma(r, D.A[2], D.A[1]);
+  const double hi = hadd(r, w);
+  const double r2 = hmul(r, r);
+  double lo = hadd(hsub(w, hi), r);
+  lo = hfma(kd, D.ln2lo, lo);
+  const double r3 = hmul(r, r2);
+  const double p2 = hfma(r, D.A[4], D.A[3]);
+  const double t = hfma(r2, D.A[0], lo);
+  const double q = hfma(p2, r2, p1);
+  const double y = hfma(r3, q, t);
+  return hadd(y, hi);
+}
+__device__ __forceinline__ bool log_main_ok(double x) {
+  const unsigned long long ix = as_u64(x);
+  const unsigned top = static_cast<unsigned>(ix >> 48);
+  return !(ix - 0x3fee000000000000ull <= 0x308ffffffffffull) && !(top - 0x10u > 0x7fdfu);
+}
+
+// two K1 series (core.cpp:28-47) in one loop; a value stops updating at its own exit
+__device__ __forceinline__ void bessel_k1_series_x2(double x0, double x1, double& k0, double& k1) {
+  const double q0 = hmul(hmul(0.25, x0), x0), q1 = hmul(hmul(0.25, x1), x1);
+  double t0 = 1.0, t1 = 1.0, si0 = 0.0, si1 = 0.0, sk0 = 0.0, sk1 = 0.0;
+  bool a0 = true, a1 = true;
+  for (int j = 0; j < 64 && (a0 || a1); ++j) {
+    const double psi = kK1Dev.psi[j], den = kK1Dev.den[j], rden = kK1Dev.rden[j];
+    const double ni0 = hadd(si0, t0), ni1 = hadd(si1, t1);
+    const double nk0 = hadd(sk0, hmul(psi, t0)), nk1 = hadd(sk1, hmul(psi, t1));
+    const double nx0 = div_by_const(hmul(t0, q0), den, rden), nx1 = div_by_const(hmul(t1, q1), den, rden);
+    if (a0) {
+      si0 = ni0;
+      sk0 = nk0;
+      if (nx0 < hmul(1e-19, hadd(si0, 1.0))) a0 = false;
+      else t0 = nx0;
+    }
+    if (a1) {
+      si1 = ni1;
+      sk1 = nk1;
+      if (nx1 < hmul(1e-19, hadd(si1, 1.0))) a1 = false;
+      else t1 = nx1;
+    }
+  }
+  const double i10 = hmul(hmul(0.5, x0), si0), i11 = hmul(hmul(0.5, x1), si1);
+  const double h0 = hmul(0.5, x0), h1 = hmul(0.5, x1);
+  double l0 = log_main(h0), l1 = log_main(h1);
+  if (!log_main_ok(h0)) l0 = glibc_log(h0);
+  if (!log_main_ok(h1)) l1 = glibc_log(h1);
+  k0 = hsub(hadd(__drcp_rn(x0), hmul(l0, i10)), hmul(hmul(0.25, x0), sk0));
+  k1 = hsub(hadd(__drcp_rn(x1), hmul(l1, i11)), hmul(hmul(0.25, x1), sk1));
+}
+
+// phi for two squared distances (core.hpp:71-74, core.cpp:130-134); KIND 0 Gaussian, 1 Matern
+template <int KIND>
+__device__ __forceinline__ void phi_x2(const KernelParams& kp, double r2a, double r2b, double& fa, double& fb) {
+  if constexpr (KIND == 0) {
+    glibc_exp_x2(-r2a, -r2b, fa, fb);
+  } else {
+    const double ra = hm_sqrt(r2a), rb = hm_sqrt(r2b);
+    if (ra <= 2.0 && rb <= 2.0) {
+      double ka, kb;
+      bessel_k1_series_x2(ra, rb, ka, kb);
+      fa = hmul(hmul(ka, ra), kp.matern_norm);
+      fb = hmul(hmul(kb, rb), kp.matern_norm);
+    } else {
+      fa = r2a == 0.0 ? kp.matern_norm : hmul(hmul(bessel_k1(ra), ra), kp.matern_norm);
+      fb = r2b == 0.0 ? kp.matern_norm : hmul(hmul(bessel_k1(rb), rb), kp.matern_norm);
+      return;
+    }
+    if (r2a == 0.0) fa = kp.matern_norm;
+    if (r2b == 0.0) fb = kp.matern_norm;
+  }
+}
+#endif
 
 // r2 over d axes of SoA coordinates (stride = n), reference axis order.
 template <int DIM>

@@ -244,3 +244,21 @@ def test_config5_full_size_row_sampled_and_block_cg(gpu, oracle):
     assert single.iterations == 2
     assert np.array_equal(bits(single.x), bits(X[:, 0]))
     assert single.relative_residual == res[0]
+
+
+def test_batch_sweep_csv(gpu):
+    """tools/hmat_csv.py --command batch-sweep writes the reference CLI's batch-sweep CSV
+    (hmat_cli.cpp:241-283): header, bs_aca rows (phase aca) then bs_dense rows (phase dense)."""
+    import subprocess
+    import sys
+    repo = os.path.dirname(HERE)
+    out = subprocess.run([sys.executable, os.path.join(repo, "tools", "hmat_csv.py"), "--command", "batch-sweep",
+                          "--n", "2048", "--c-leaf", "64", "--trials", "2"], check=True, capture_output=True,
+                         text=True).stdout.splitlines()
+    assert out[0] == "bs,phase,n,d,k,c_leaf,time_ms_mean,time_ms_min"
+    rows = [r.split(",") for r in out[1:]]
+    assert [r[1] for r in rows] == ["aca"] * 6 + ["dense"] * 6
+    assert [int(r[0]) for r in rows[:6]] == [0] + [1 << e for e in range(14, 23, 2)]
+    assert [int(r[0]) for r in rows[6:]] == [0] + [1 << e for e in range(16, 25, 2)]
+    assert all(r[2:6] == ["2048", "2", "16", "64"] for r in rows)
+    assert all(float(r[6]) > 0 and float(r[7]) > 0 for r in rows)

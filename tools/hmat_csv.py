@@ -10,6 +10,10 @@ these.  Commands (hmat_cli.cpp:117-255, 410-441):
   convergence kernel,d,k,e_rel_mean                             (k = 2, 4, 8, 16; no N limit:
                                                                  the exact product runs on the GPU)
   solve       one value of x per line (17 digits); iterations / residual on stderr
+  batch-sweep bs,phase,n,d,k,c_leaf,time_ms_mean,time_ms_min    (bs_aca sweep: 0, 2^14..2^22 step 4x,
+                                                                 phase aca; bs_dense sweep: 0,
+                                                                 2^16..2^24 step 4x, phase dense;
+                                                                 hmat_cli.cpp:241-283)
 
 mvp_dense / mvp_aca come from the per-kernel event clock: the near-field kernels and the
 far-field kernels (ACA factorisation included in recompute mode) of one product.
@@ -147,9 +151,41 @@ def cmd_solve(a, out):
     print(f"iterations {r.iterations}, relative residual {r.relative_residual:g}", file=sys.stderr)
 
 
+def cmd_batch_sweep(a, out):
+    """hmat_cli.cpp:241-283: MvpTimings aca_ms / dense_ms of `trials` products per batch
+    size (recompute mode unless --precompute).  On the device bs_aca sets the reference's
+    ACA batches, chunks are runs of whole batches; bs_dense only bounds the block size."""
+    kern = hm.KernelFunction(a.kernel)
+    P = halton_points(a.n, a.d)
+    x = symmetric(a.seed, a.n)
+    out.append("bs,phase,n,d,k,c_leaf,time_ms_mean,time_ms_min")
+
+    def measure(bs_aca, bs_dense):
+        h = hm.setup(P, kern, config(a, bs_aca=bs_aca, bs_dense=bs_dense))
+        aca, dense = [], []
+        for _ in range(a.trials):
+            t = hm.MvpTimings()
+            h.mvp(x, t)
+            aca.append(t.aca_ms)
+            dense.append(t.dense_ms)
+        h.close()
+        return aca, dense
+
+    sweep = [0] + [1 << e for e in range(14, 23, 2)]
+    for bs in sweep:
+        aca, _ = measure(bs, a.bs_dense)
+        out.append(",".join([g(bs), "aca", g(a.n), g(a.d), g(a.k), g(a.c_leaf), g(summarize(aca)[0]), g(min(aca))]))
+    sweep = [0] + [1 << e for e in range(16, 25, 2)]
+    for bs in sweep:
+        _, dense = measure(a.bs_aca, bs)
+        out.append(",".join([g(bs), "dense", g(a.n), g(a.d), g(a.k), g(a.c_leaf), g(summarize(dense)[0]),
+                             g(min(dense))]))
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser(description="reference-CLI-compatible CSV outputs")
-    ap.add_argument("--command", required=True, choices=["mvp-bench", "complexity", "convergence", "solve"])
+    ap.add_argument("--command", required=True, choices=["mvp-bench", "complexity", "convergence", "solve",
+                                                               "batch-sweep"])
     ap.add_argument("--n", type=int, default=8192)
     ap.add_argument("--d", type=int, default=2)
     ap.add_argument("--kernel", default="gaussian", choices=["gaussian", "matern"])
@@ -172,7 +208,7 @@ def main(argv=None):
     a = ap.parse_args(argv)
     out: list[str] = []
     {"mvp-bench": cmd_mvp_bench, "complexity": cmd_complexity, "convergence": cmd_convergence,
-     "solve": cmd_solve}[a.command](a, out)
+     "solve": cmd_solve, "batch-sweep": cmd_batch_sweep}[a.command](a, out)
     text = "\n".join(out) + "\n"
     if a.out:
         with open(a.out, "w") as f:  # rows collected first: no partial files (hmat_cli.cpp:104-106)
