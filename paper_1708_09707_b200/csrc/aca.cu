@@ -90,8 +90,10 @@ void compute_aca(HMatrix& h, const AcaChunk& c, cudaStream_t s) {
   if (cnt <= 0) return;
   PhaseTrace tr;
   tr.mark("start", s);
-  if (h.aca_counters.size() < static_cast<size_t>(kAcaClasses)) h.aca_counters.alloc(kAcaClasses, s);
+  // [0, K) job counters, [K, 2K) fallback counts, [2K, 3K) fallback job counters
+  if (h.aca_counters.size() < static_cast<size_t>(3 * kAcaClasses)) h.aca_counters.alloc(3 * kAcaClasses, s);
   h.aca_counters.zero(s);
+  if (h.aca_fallback.size() < static_cast<size_t>(cnt)) h.aca_fallback.alloc(cnt, s);
   if (h.aca_rej.size() < 2) reset_aca_rejections(h, s);
   AcaJob J{};
   J.rl = h.aca.rl.get();
@@ -147,6 +149,16 @@ void compute_aca(HMatrix& h, const AcaChunk& c, cudaStream_t s) {
   L.device = h.device;
   L.big_scratch = &h.aca_big_scratch;
   L.tr = &tr;
+  // smooth-path kernels: by default for d >= 3 (no noise floor);
+  // HM_SMOOTH=0/1 forces them off/on (results are bitwise identical either way)
+  {
+    const char* e = std::getenv("HM_SMOOTH");
+    L.smooth = (e ? std::atoi(e) != 0 : h.d >= 3) && h.cfg.k == 16 && h.d <= 4;
+  }
+  L.fb_list = h.aca_fallback.get();
+  L.fb_count = h.aca_counters.get() + kAcaClasses;
+  L.fb_counter = h.aca_counters.get() + 2 * kAcaClasses;
+  for (int q = 0; q <= kAcaClasses; ++q) L.first[q] = first[q];
   switch (h.d) {
     case 1: aca_classes_d1(L, s); break;
     case 2: aca_classes_d2(L, s); break;

@@ -5,6 +5,8 @@
 // then the window kernels from the largest class down (largest-first within a class).
 #include "aca_impl.cuh"
 
+#include <type_traits>
+
 #ifndef HM_ACA_DIM
 #error "compile with -DHM_ACA_DIM=<0..4>"
 #endif
@@ -38,6 +40,32 @@ static void classes_kind(const AcaClassLaunch& L, cudaStream_t s) {
     tr.mark("win NW=16 (<=1024)", s);
     launch_win<DIM, KIND, 8, 16, 8, true, 2>(L.J[3], E, sms, s);
     tr.mark("NW=8 (<=512)", s);
+    if constexpr (DIM > 0) {
+      if (L.smooth) {
+        // smooth-path kernels, then the general window kernel over the blocks they handed back
+        auto smooth_then_window = [&](auto nwc, int q) {
+          constexpr int NWq = decltype(nwc)::value;
+          AcaJob Js = L.J[q];
+          Js.fb_list = L.fb_list + L.first[q];
+          Js.fb_count = L.fb_count + q;
+          launch_smooth<DIM, KIND, NWq>(Js, E, sms, s);
+          AcaJob Jw = L.J[q];
+          Jw.order = Js.fb_list;
+          Jw.njobs_dev = Js.fb_count;
+          Jw.counter = L.fb_counter + q;
+          if constexpr (NWq == 4) launch_win<DIM, KIND, 4, 16, 16, true, 3>(Jw, E, sms, s);
+          else if constexpr (NWq == 2) launch_win<DIM, KIND, 2, 16, 16, true, 3>(Jw, E, sms, s);
+          else launch_win<DIM, KIND, 1, 16, 8, true, 3>(Jw, E, sms, s);
+        };
+        smooth_then_window(std::integral_constant<int, 4>{}, 2);
+        tr.mark("smooth NW=4 (<=256)", s);
+        smooth_then_window(std::integral_constant<int, 2>{}, 1);
+        tr.mark("smooth NW=2 (<=128)", s);
+        smooth_then_window(std::integral_constant<int, 1>{}, 0);
+        tr.mark("smooth NW=1 (<=64)", s);
+        return;
+      }
+    }
     launch_win<DIM, KIND, 4, 16, 16, true, 3>(L.J[2], E, sms, s);
     tr.mark("NW=4 (<=256)", s);
     // the small blocks are latency-bound: registers capped for 12 warps per SM (ncu: at

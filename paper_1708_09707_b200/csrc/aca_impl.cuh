@@ -182,6 +182,9 @@ struct AcaJob {
   unsigned long long* rejections;
   unsigned long long* evals;  // optional (HM_TRACE): [0] column-scan entries, [1] pivot-row entries, [2] blocks
   int tile_shift;           // -1: U rank-major; else log2(S), U row-tiled by S rows
+  const int* njobs_dev = nullptr;  // job count on the device (fallback lists), overrides njobs
+  int* fb_list = nullptr;   // smooth kernel: blocks that hit a rejection are appended here
+  int* fb_count = nullptr;
   // explicit-matrix seam: block b entries at dense + dense_off[b], row-major m x n
   const double* dense;
   const long long* dense_off;
@@ -460,6 +463,30 @@ void launch_kernel_aca(const AcaJob& J, const KernelEntry<DIM>& E, int sms, cuda
   HM_LAUNCH_CHECK();
 }
 
+// Window columns receive the new cross: dst_c[i] -= u_r[i] * v_r[c] for the `filled`
+// window columns c.  Batches of 4 columns: the v_r values and the window entries of a
+// batch are loaded before any store, so the loads overlap (the compiler cannot hoist
+// them across the stores of a plain loop: same array).
+template <int RPL, class VAT, class DST>
+__device__ __forceinline__ void window_cross(int filled, int next, const double (&ur)[RPL], const bool (&rv)[RPL],
+                                             int t, int TT, VAT vat_r, DST dst_of) {
+  for (int c0 = 0; c0 < filled; c0 += 4) {
+    double vr[4], a[4][RPL];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) vr[c] = c0 + c < filled ? vat_r(next + c0 + c) : 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int q = 0; q < RPL; ++q)
+        a[c][q] = (c0 + c < filled && rv[q]) ? dst_of(next + c0 + c)[t + q * TT] : 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int q = 0; q < RPL; ++q)
+        if (c0 + c < filled && rv[q]) dst_of(next + c0 + c)[t + q * TT] = hsub(a[c][q], hmul(ur[q], vr[c]));
+  }
+}
+
 // Team barrier: a warp (NW = 1) or a named barrier over the team's NW warps.
 template <int NW>
 __device__ __forceinline__ void team_sync(int team) {
@@ -520,7 +547,7 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
     team_sync<NW>(team);
     const long long job = static_cast<long long>(s_misc[0]);
     team_sync<NW>(team);
-    if (job >= J.njobs) return;
+    if (job >= (J.njobs_dev ? static_cast<long long>(*J.njobs_dev) : J.njobs)) return;
     const int b = J.order[job];
     const int rl = J.rl[b], m = J.m[b], cl = J.cl[b], n = J.nn[b];
     double* U = J.U + (J.u_off[b] - J.u_base);
@@ -818,13 +845,12 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
       team_sync<NW>(team);
       if (t == pt) s_used[p] = 1;  // after every reader of the old flag (argmax above)
       // window columns receive this cross (next step of their chain)
-      for (int co = 0; co < filled; ++co) {
-        const int col = next + co;
-        const double vr = vat(r, col);
-        double* dst = s_win + (col % W) * PS;
+      {
+        double ur[RPL];
 #pragma unroll
-        for (int q = 0; q < RPL; ++q)
-          if (rv[q]) dst[t + q * TT] = hsub(dst[t + q * TT], hmul(uR[q][KC - 1], vr));
+        for (int q = 0; q < RPL; ++q) ur[q] = uR[q][KC - 1];
+        window_cross<RPL>(filled, next, ur, rv, t, TT, [&](int col) { return vat(r, col); },
+                          [&](int col) { return s_win + (col % W) * PS; });
       }
       if (t == 0) {
         J.row_piv[static_cast<long long>(b) * kmax + r] = p;
@@ -894,6 +920,262 @@ void launch_win(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, cudaS
 }
 
 // ---------------------------------------------------------------------------
+// Smooth-path kernel (max(m, n) <= 64 NW, k = 16): the regime of every block in d >= 3
+// (no candidate column is ever rejected), where the batched ACA is
+// a fixed schedule -- the candidate column at rank r is column r.  A team of NW warps
+// per block, lane-owned rows i = t, t + 64 NW/2 (u_l of its rows LEFT-aligned in
+// registers: no per-rank shifting) and columns j = t, t + 32 NW.
+//   * the k raw candidate columns A(:, c) are evaluated up front, all rows at once
+//     (independent evaluations, off the per-rank critical path), into shared memory;
+//   * per rank: the column's residual chain, ONE fused reduction (norm2 for the
+//     qualification test, nonzero flag, argmax over unused rows), the pivot export,
+//     u_r, then the pivot row's entries and chain for two columns per thread;
+//   * scale2 is a bracket of the parallel norm until a decision needs it exactly.
+// If a candidate column is not qualified (a rejection: noise floor, zero column) the
+// block is handed to the general window kernel through a fallback list and recomputed
+// there from scratch, so every block's factors are bitwise the reference's either way.
+template <int NW>
+__host__ __device__ constexpr size_t smooth_stride() {
+  return static_cast<size_t>(16) * (NW * 64 + 1) + static_cast<size_t>(16) * NW * 64 + 16 + 4 + 4 * NW + 8;
+}
+
+template <int DIM, int KIND, int NW>
+__global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntry<DIM, KIND> E, int teams_per_cta) {
+  constexpr int KC = 16;
+  constexpr int TT = NW * 32, NCAP = 2 * TT, CS = NCAP + 1;
+  static_assert(DIM > 0, "smooth kernel: compile-time dimension");
+  extern __shared__ double smem[];
+  const int team = threadIdx.x / TT, t = threadIdx.x % TT, lane = t & 31, wib = t >> 5;
+  if (team >= teams_per_cta) return;
+  double* base = smem + static_cast<size_t>(team) * smooth_stride<NW>();
+  double* s_col = base;                 // KC x CS: raw candidate columns A(i, c)
+  double* s_v = s_col + KC * CS;        // KC x NCAP: v_l[j]
+  double* s_up = s_v + KC * NCAP;       // KC: u_l[p]
+  double* s_yp = s_up + KC;             // the pivot row's point
+  double* s_red = s_yp + 4;             // NW x 4: per-warp sum, nz, bv, bi
+  double* s_misc = s_red + 4 * NW;      // [0] job [1] pivot value [2] exact verdict [3] scale
+  const double kEps0sq = 1e-14 * 1e-14;
+  const int kmax = J.kmax;
+
+  for (;;) {
+    if (t == 0) s_misc[0] = static_cast<double>(atomicAdd(J.counter, 1));
+    team_sync<NW>(team);
+    const long long job = static_cast<long long>(s_misc[0]);
+    team_sync<NW>(team);
+    if (job >= J.njobs) return;
+    const int b = J.order[job];
+    const int rl = J.rl[b], m = J.m[b], cl = J.cl[b], n = J.nn[b];
+    const bool rv0 = t < m, rv1 = t + TT < m;
+    double y0[DIM], y1[DIM];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      y0[a] = rv0 ? __ldg(E.coords + a * E.n + rl + t) : 0.0;
+      y1[a] = rv1 ? __ldg(E.coords + a * E.n + rl + t + TT) : 0.0;
+    }
+    // raw candidate columns 0 .. min(k, n) - 1, two columns (four entries) at a time
+    const int ncol = min(kmax, n);
+    for (int c = 0; c < ncol; c += 2) {
+      const int c1 = c + 1 < ncol ? c + 1 : c;
+      double a0, a1, b0, b1;
+      E.eval2(y0, y1, cl + c, a0, a1);
+      E.eval2(y0, y1, cl + c1, b0, b1);
+      s_col[c * CS + t] = a0;
+      s_col[c * CS + t + TT] = a1;
+      s_col[c1 * CS + t] = b0;
+      s_col[c1 * CS + t + TT] = b1;
+    }
+    team_sync<NW>(team);
+    double uR0[KC], uR1[KC];
+#pragma unroll
+    for (int l = 0; l < KC; ++l) uR0[l] = uR1[l] = 0.0;
+    bool used0 = false, used1 = false;
+    double s_lo = 0.0, s_hi = 0.0, scale = 0.0;
+    bool scale_exact = false;
+    const double gm = static_cast<double>(m) * 1.2e-16;
+    int k_eff = 0;
+    bool fallback = false;
+    for (int r = 0; r < kmax; ++r) {
+      if (r >= n) break;  // no candidate column left: converged (aca.cpp:442-443)
+      // column r residual (aca.cpp:363-364), rows of this thread
+      double a0 = s_col[r * CS + t], a1 = rv1 ? s_col[r * CS + t + TT] : 0.0;
+      SmoothChain<KC>::col2<NCAP>(a0, a1, uR0, uR1, r, s_v + r);
+      // fused reduction: norm2 (any order, bounded), nonzero flag, argmax over unused rows
+      double sum = 0.0, bv = -1.0;
+      int nz = 0, bi = 0x7fffffff;
+      if (rv0) {
+        sum = hmul(a0, a0);
+        if (!used0) {
+          nz |= fabs(a0) > 0.0 ? 1 : 0;
+          bv = fabs(a0);
+          bi = t;
+        }
+      }
+      if (rv1) {
+        sum = hadd(sum, hmul(a1, a1));
+        if (!used1) {
+          nz |= fabs(a1) > 0.0 ? 1 : 0;
+          argmax_combine(bv, bi, fabs(a1), t + TT);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+        nz |= __shfl_xor_sync(0xffffffffu, nz, o);
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        argmax_combine(bv, bi, ov, oi);
+      }
+      if constexpr (NW > 1) {
+        if (lane == 0) {
+          s_red[4 * wib] = sum;
+          s_red[4 * wib + 1] = static_cast<double>(nz);
+          s_red[4 * wib + 2] = bv;
+          s_red[4 * wib + 3] = static_cast<double>(bi);
+        }
+        team_sync<NW>(team);
+        sum = s_red[0];
+        nz = static_cast<int>(s_red[1]);
+        bv = s_red[2];
+        bi = static_cast<int>(s_red[3]);
+        for (int w = 1; w < NW; ++w) {
+          sum = hadd(sum, s_red[4 * w]);
+          nz |= static_cast<int>(s_red[4 * w + 1]);
+          argmax_combine(bv, bi, s_red[4 * w + 2], static_cast<int>(s_red[4 * w + 3]));
+        }
+      }
+      // qualification (aca.cpp:381-383): best > 0 and (first cross or norm2 > 1e-28 scale2)
+      int st = 0;
+      if (nz) {
+        if (r == 0) {
+          st = 1;
+        } else {
+          const double Tlo = hmul(kEps0sq, scale_exact ? scale : s_lo);
+          const double Thi = hmul(kEps0sq, scale_exact ? scale : s_hi);
+          const double lo = hmul(sum, 1.0 - 4.0 * gm), hi = hmul(sum, 1.0 + 4.0 * gm);
+          st = lo > Thi ? 1 : (hi <= Tlo ? 0 : 2);
+        }
+      }
+      if (st == 2) {  // inside the bound: the reference's sequential left folds
+        if (rv0) s_col[r * CS + t] = a0;  // raw column r is no longer needed
+        if (rv1) s_col[r * CS + t + TT] = a1;
+        team_sync<NW>(team);
+        if (t == 0) {
+          if (!scale_exact) {  // scale2 = left fold of the first accepted column, A(:, 0)
+            double f = hmul(s_col[0], s_col[0]);
+            for (int i = 1; i < m; ++i) f = hadd(f, hmul(s_col[i], s_col[i]));
+            s_misc[3] = f;
+          }
+          const double sc = scale_exact ? scale : s_misc[3];
+          double f = hmul(s_col[r * CS], s_col[r * CS]);
+          for (int i = 1; i < m; ++i) f = hadd(f, hmul(s_col[r * CS + i], s_col[r * CS + i]));
+          s_misc[2] = f > hmul(kEps0sq, sc) ? 1.0 : 0.0;
+        }
+        team_sync<NW>(team);
+        if (!scale_exact) {
+          scale = s_misc[3];
+          scale_exact = true;
+        }
+        st = s_misc[2] != 0.0 ? 1 : 0;
+        team_sync<NW>(team);
+      }
+      if (st != 1) {  // a rejection: the general kernel takes the block
+        fallback = true;
+        break;
+      }
+      if (r == 0) {  // scale2 (aca.cpp:491) bracketed by the parallel norm of column 0
+        s_lo = hmul(sum, 1.0 - 4.0 * gm);
+        s_hi = hmul(sum, 1.0 + 4.0 * gm);
+      }
+      const int p = bi;
+      // the pivot row's owner exports u_l[p], the pivot value and its point
+      if (t == (p % TT)) {
+        const bool q1 = p >= TT;
+#pragma unroll
+        for (int l = 0; l < KC; ++l)
+          if (l < r) s_up[l] = q1 ? uR1[l] : uR0[l];
+        s_misc[1] = q1 ? a1 : a0;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) s_yp[a] = q1 ? y1[a] : y0[a];
+        if (q1) used1 = true;
+        else used0 = true;
+      }
+      team_sync<NW>(team);
+      const PivotDiv pdiv(s_misc[1]);
+      SmoothChain<KC>::put(uR0, r, rv0 ? pdiv(a0) : 0.0);  // u_r = u_hat / pivot (aca.cpp:466-470)
+      SmoothChain<KC>::put(uR1, r, rv1 ? pdiv(a1) : 0.0);
+      // pivot row: v_r[j] = A(p, j) - sum_l u_l[p] v_l[j] (aca.cpp:474-481), columns t, t + TT
+      {
+        double yp[DIM];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) yp[a] = s_yp[a];
+        const int j0 = t, j1 = t + TT;
+        const bool cv0 = j0 < n, cv1 = j1 < n;
+        double b0, b1;
+        E.eval2c(yp, cl + (cv0 ? j0 : 0), cl + (cv1 ? j1 : 0), b0, b1);
+        SmoothChain<KC>::row2<NCAP>(b0, b1, s_up, s_v + j0, s_v + j1, r);
+        if (cv0) s_v[r * NCAP + j0] = b0;
+        if (cv1) s_v[r * NCAP + j1] = b1;
+      }
+      if (t == 0) {
+        J.row_piv[static_cast<long long>(b) * kmax + r] = p;
+        J.col_piv[static_cast<long long>(b) * kmax + r] = r;
+      }
+      k_eff = r + 1;
+      team_sync<NW>(team);
+    }
+    if (fallback) {
+      if (t == 0) J.fb_list[atomicAdd(J.fb_count, 1)] = b;
+      team_sync<NW>(team);
+      continue;
+    }
+    // factors: U (layout uix, zero past k_eff), V interleaved n x kmax
+    double* U = J.U + (J.u_off[b] - J.u_base);
+    double* V = J.V + (J.v_off[b] - J.v_base);
+    const int tsh = J.tile_shift;
+    auto uix = [&](int l, int i) -> long long {
+      if (tsh < 0) return static_cast<long long>(l) * m + i;
+      return ((static_cast<long long>(i >> tsh) * kmax + l) << tsh) + (i & ((1 << tsh) - 1));
+    };
+#pragma unroll
+    for (int l = 0; l < KC; ++l) {
+      if (rv0) U[uix(l, t)] = l < k_eff ? uR0[l] : 0.0;
+      if (rv1) U[uix(l, t + TT)] = l < k_eff ? uR1[l] : 0.0;
+    }
+    for (int idx = t; idx < n * KC; idx += TT) {
+      const int j = idx >> 4, l = idx & 15;
+      V[idx] = l < k_eff ? s_v[l * NCAP + j] : 0.0;
+    }
+    for (int l = k_eff + t; l < kmax; l += TT) {
+      J.row_piv[static_cast<long long>(b) * kmax + l] = -1;
+      J.col_piv[static_cast<long long>(b) * kmax + l] = -1;
+    }
+    if (t == 0) {
+      J.k_eff[b] = k_eff;
+      if (J.evals) {
+        atomicAdd(J.evals, static_cast<unsigned long long>(ncol) * m);
+        atomicAdd(J.evals + 1, static_cast<unsigned long long>(k_eff) * n);
+        atomicAdd(J.evals + 2, 1ull);
+      }
+    }
+    team_sync<NW>(team);
+  }
+}
+
+template <int DIM, int KIND, int NW>
+void launch_smooth(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, cudaStream_t s) {
+  if (J.njobs <= 0) return;
+  constexpr int teams = 4 / NW;
+  const size_t smem = teams * smooth_stride<NW>() * sizeof(double);
+  auto kfn = aca_smooth_kernel<DIM, KIND, NW>;
+  HM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int occ = 0;
+  HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 128, smem));
+  const long long ctas = std::min<long long>((J.njobs + teams - 1) / teams, static_cast<long long>(std::max(occ, 1)) * sms);
+  kfn<<<static_cast<unsigned>(std::max(ctas, 1ll)), 128, smem, s>>>(J, E, teams);
+  HM_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
 // Big-block kernel (max(m, n) > 1024): one 256-thread CTA per block, rows strided
 // over the CTA in pairs.  The window of W candidate columns lives in a per-CTA
 // global scratch (L2-resident: W x m doubles); for each row pair a thread loads
@@ -918,6 +1200,7 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
   int* s_rbi = reinterpret_cast<int*>(s_rbv + 8);
   int* s_state = reinterpret_cast<int*>(s_rbv + 12);
   double* s_misc = s_rbv + 20;  // [0] job [1] scale [2] verdict
+  double* s_wsum = s_misc + 4;  // W: parallel norm of each window column
   const int t = threadIdx.x, lane = t & 31, wib = t >> 5;
   const double kEps0sq = 1e-14 * 1e-14;
   const int kmax = J.kmax;
@@ -944,11 +1227,45 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
 
     int next = 0, filled = 0, k_eff = 0;
     unsigned long long rejections = 0, ev_col = 0, ev_row = 0;
-    double scale = -1.0;
+    // scale2 = norm2 of the first accepted column (aca.cpp:491): a bracket [s_lo, s_hi] of
+    // its parallel sum until a decision falls inside it, then the exact left fold
+    double scale = -1.0, s_lo = 0.0, s_hi = 0.0;
+    bool have_scale = false, scale_exact = false;
+    int c0col = 0;
     const double gm = static_cast<double>(m) * 1.2e-16;
+    auto decide = [&](double sum, int nz) -> int {
+      if (!nz) return 0;
+      if (!have_scale) return 1;
+      const double Tlo = hmul(kEps0sq, scale_exact ? scale : s_lo);
+      const double Thi = hmul(kEps0sq, scale_exact ? scale : s_hi);
+      const double lo = hmul(sum, 1.0 - 4.0 * gm), hi = hmul(sum, 1.0 + 4.0 * gm);
+      return lo > Thi ? 1 : (hi <= Tlo ? 0 : 2);
+    };
+    // exact scale2 on demand: the first accepted column carried no cross, so its entries are
+    // A(:, c0col) -- re-evaluated (bitwise the same) into U's next rank slot, folded in order
+    int r_cur = 0;
+    auto resolve_exact = [&]() {
+      if (scale_exact) return;
+      for (int i = t; i < m; i += TT) {
+        double y0[YD];
+        E.load(rl + i, y0);
+        U[uix(r_cur, i)] = E.eval(y0, cl + c0col);
+      }
+      __syncthreads();
+      if (t == 0) {
+        double f = hmul(U[uix(r_cur, 0)], U[uix(r_cur, 0)]);
+        for (int i = 1; i < m; ++i) f = hadd(f, hmul(U[uix(r_cur, i)], U[uix(r_cur, i)]));
+        s_misc[1] = f;
+      }
+      __syncthreads();
+      scale = s_misc[1];
+      scale_exact = true;
+    };
 
     for (int r = 0; r < kmax; ++r) {
       int acc_w = -1;
+      double acc_sum = 0.0;
+      r_cur = r;
       while (next < n) {
         // speculation depth: while no column was rejected, at most kmax - r more can be
         // accepted (smooth blocks, d >= 3: no noise floor), so do not evaluate past them
@@ -982,55 +1299,106 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
         }
         filled = wcols;
         __syncthreads();
-        {
-          const int w = wib;  // G == 32: warp w scans window column w
+        // qualification.  Fast path while the block has rejected nothing: the first window
+        // column with the whole CTA (4 loads in flight per thread); otherwise one warp per
+        // window column.  Decisions use the rigorous bound of the parallel sums; scale2 is a
+        // bracket until an ambiguous decision needs it exactly (resolve_exact).
+        int first_state = -1;
+        if (rejections == 0) {
+          const double* src = win + static_cast<long long>(next % W) * PS;
           double sum = 0.0;
           int nz = 0;
-          if (w < wcols) {
-            const double* src = win + static_cast<long long>((next + w) % W) * PS;
-            for (int i = lane; i < m; i += 32) {
-              const double a = src[i];
-              sum = hadd(sum, hmul(a, a));
-              nz |= (!is_used(i) && fabs(a) > 0.0) ? 1 : 0;
-            }
+          for (int i = t; i < m; i += 4 * TT) {
+            double a[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[u] = i + u * TT < m ? src[i + u * TT] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (i + u * TT < m) {
+                sum = hadd(sum, hmul(a[u], a[u]));
+                nz |= (!is_used(i + u * TT) && fabs(a[u]) > 0.0) ? 1 : 0;
+              }
           }
 #pragma unroll
           for (int o = 16; o; o >>= 1) {
             sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
             nz |= __shfl_xor_sync(0xffffffffu, nz, o);
           }
-          if (lane == 0 && w < wcols) {
-            int st = 0;
-            if (nz) {
-              if (scale < 0.0) {
-                st = 1;
-              } else {
-                const double T = hmul(kEps0sq, scale);
-                const double lo = hmul(sum, 1.0 - 4.0 * gm), hi = hmul(sum, 1.0 + 4.0 * gm);
-                st = lo > T ? 1 : (hi <= T ? 0 : 2);
-              }
-            }
-            s_state[w] = st;
+          if (lane == 0) {
+            s_rbv[wib] = sum;
+            s_rbi[wib] = nz;
+          }
+          __syncthreads();
+          sum = s_rbv[0];
+          nz = s_rbi[0];
+          for (int g = 1; g < TT / 32; ++g) {
+            sum = hadd(sum, s_rbv[g]);
+            nz |= s_rbi[g];
+          }
+          __syncthreads();
+          first_state = decide(sum, nz);
+          if (first_state == 1) {
+            acc_w = 0;
+            acc_sum = sum;
           }
         }
-        __syncthreads();
-        for (int w = 0; w < wcols; ++w) {
-          int st = s_state[w];
-          if (st == 2) {
-            if (t == 0) {
+        if (acc_w < 0) {
+          {
+            const int w = wib;  // G == 32: warp w scans window column w
+            double sum = 0.0;
+            int nz = 0;
+            if (w < wcols) {
               const double* src = win + static_cast<long long>((next + w) % W) * PS;
-              double f = hmul(src[0], src[0]);
-              for (int i = 1; i < m; ++i) f = hadd(f, hmul(src[i], src[i]));
-              s_misc[2] = f > hmul(kEps0sq, scale) ? 1.0 : 0.0;
+              for (int i = lane; i < m; i += 4 * 32) {
+                double a[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) a[u] = i + 32 * u < m ? src[i + 32 * u] : 0.0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                  if (i + 32 * u < m) {
+                    sum = hadd(sum, hmul(a[u], a[u]));
+                    nz |= (!is_used(i + 32 * u) && fabs(a[u]) > 0.0) ? 1 : 0;
+                  }
+              }
             }
-            __syncthreads();
-            st = s_misc[2] != 0.0 ? 1 : 0;
-            __syncthreads();
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+              sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+              nz |= __shfl_xor_sync(0xffffffffu, nz, o);
+            }
+            if (lane == 0 && w < wcols) {
+              s_state[w] = decide(sum, nz);
+              s_wsum[w] = sum;
+            }
           }
-          if (st == 1) {
-            acc_w = w;
-            break;
+          __syncthreads();
+          for (int w = 0; w < wcols; ++w) {
+            int st = s_state[w];
+            if (st == 2) {
+              resolve_exact();
+              if (t == 0) {  // the reference's sequential left fold (aca.cpp:373-374 / 414-415)
+                const double* src = win + static_cast<long long>((next + w) % W) * PS;
+                double f = hmul(src[0], src[0]);
+                for (int i = 1; i < m; ++i) f = hadd(f, hmul(src[i], src[i]));
+                s_misc[2] = f > hmul(kEps0sq, scale) ? 1.0 : 0.0;
+              }
+              __syncthreads();
+              st = s_misc[2] != 0.0 ? 1 : 0;
+              __syncthreads();
+            }
+            if (st == 1) {
+              acc_w = w;
+              acc_sum = s_wsum[w];
+              break;
+            }
           }
+        }
+        if (!have_scale && acc_w >= 0) {
+          // first cross: scale2 (aca.cpp:491) bracketed by the parallel norm of the column
+          s_lo = hmul(acc_sum, 1.0 - 4.0 * gm);
+          s_hi = hmul(acc_sum, 1.0 + 4.0 * gm);
+          c0col = next + acc_w;
+          have_scale = true;
         }
         const int consumed = acc_w >= 0 ? acc_w + 1 : wcols;
         rejections += static_cast<unsigned long long>(acc_w >= 0 ? acc_w : wcols);
@@ -1043,12 +1411,19 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
       const double* acol = win + static_cast<long long>(cstar % W) * PS;
       double bv = -1.0;
       int bi = 0x7fffffff;
-      for (int i = t; i < m; i += TT) {
-        if (!is_used(i)) {
-          const double av = fabs(acol[i]);
-          if (av > bv) {
-            bv = av;
-            bi = i;
+      for (int i = t; i < m; i += 4 * TT) {
+        double a[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[u] = i + u * TT < m ? acol[i + u * TT] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int ii = i + u * TT;
+          if (ii < m && !is_used(ii)) {
+            const double av = fabs(a[u]);
+            if (av > bv) {
+              bv = av;
+              bi = ii;
+            }
           }
         }
       }
@@ -1067,18 +1442,18 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
       bi = s_rbi[0];
       for (int g = 1; g < TT / 32; ++g) argmax_combine(bv, bi, s_rbv[g], s_rbi[g]);
       const int p = bi;
-      if (t == 0) {
-        if (r == 0) {
-          double f = hmul(acol[0], acol[0]);
-          for (int i = 1; i < m; ++i) f = hadd(f, hmul(acol[i], acol[i]));
-          s_misc[1] = f;
-        }
+      if (t == 0)
         for (int l = 0; l < r; ++l) s_up[l] = U[uix(l, p)];
-      }
       __syncthreads();
-      if (r == 0) scale = s_misc[1];
       const PivotDiv pdiv(acol[p]);
-      for (int i = t; i < m; i += TT) U[uix(r, i)] = pdiv(acol[i]);
+      for (int i = t; i < m; i += 4 * TT) {
+        double a[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[u] = i + u * TT < m ? acol[i + u * TT] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i + u * TT < m) U[uix(r, i + u * TT)] = pdiv(a[u]);
+      }
       ev_row += n;
       {
         double yp[YD];
@@ -1108,11 +1483,22 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
       }
       __syncthreads();
       if (t == 0) s_mask[p >> 5] |= 1u << (p & 31);
-      for (int co = 0; co < filled; ++co) {
-        const int col = next + co;
-        const double vr = V[static_cast<long long>(col) * kmax + r];
-        double* dst = win + static_cast<long long>(col % W) * PS;
-        for (int i = t; i < m; i += TT) dst[i] = hsub(dst[i], hmul(U[uix(r, i)], vr));
+      {
+        // per row: u_r[i] once, the W window entries loaded together (the loop was a
+        // load-latency-bound chain of L2 round trips, one column at a time)
+        double vr[W];
+#pragma unroll
+        for (int co = 0; co < W; ++co) vr[co] = co < filled ? V[static_cast<long long>(next + co) * kmax + r] : 0.0;
+        for (int i = t; i < m; i += TT) {
+          const double u = U[uix(r, i)];
+          double a[W];
+#pragma unroll
+          for (int co = 0; co < W; ++co)
+            a[co] = co < filled ? win[static_cast<long long>((next + co) % W) * PS + i] : 0.0;
+#pragma unroll
+          for (int co = 0; co < W; ++co)
+            if (co < filled) win[static_cast<long long>((next + co) % W) * PS + i] = hsub(a[co], hmul(u, vr[co]));
+        }
       }
       if (t == 0) {
         J.row_piv[static_cast<long long>(b) * kmax + r] = p;
@@ -1489,13 +1875,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
       }
       cluster.sync();  // v_r visible to the whole cluster (release / acquire)
       if (cr == po && t == pt) s_used[pl] = 1;
-      for (int co = 0; co < filled; ++co) {
-        const int col = next + co;
-        const double vr = V[static_cast<long long>(col) * kmax + r];
-        double* dst = s_win + (col % W) * PS;
+      {
+        double ur[RPL];
 #pragma unroll
-        for (int q = 0; q < RPL; ++q)
-          if (rv[q]) dst[t + q * TT] = hsub(dst[t + q * TT], hmul(uR[q][KC - 1], vr));
+        for (int q = 0; q < RPL; ++q) ur[q] = uR[q][KC - 1];
+        window_cross<RPL>(filled, next, ur, rv, t, TT,
+                          [&](int col) { return V[static_cast<long long>(col) * kmax + r]; },
+                          [&](int col) { return s_win + (col % W) * PS; });
       }
       if (cr == 0 && t == 0) {
         J.row_piv[static_cast<long long>(b) * kmax + r] = p;
@@ -1606,6 +1992,11 @@ struct AcaClassLaunch {
   int device = 0;
   DevBuf<double>* big_scratch = nullptr;  // persistent window scratch of the big-block kernel
   PhaseTrace* tr = nullptr;
+  bool smooth = false;         // smooth-path kernels for the <= 256 classes (fallback lists)
+  int* fb_list = nullptr;      // per class q at offset first[q]: blocks handed back
+  int* fb_count = nullptr;     // kAcaClasses counts
+  int* fb_counter = nullptr;   // kAcaClasses job counters of the fallback passes
+  long long first[kAcaClasses + 1] = {};
 };
 void aca_classes_d0(const AcaClassLaunch& L, cudaStream_t s);
 void aca_classes_d1(const AcaClassLaunch& L, cudaStream_t s);

@@ -143,6 +143,7 @@ struct HMatrix : HandleStreams {
   DevBuf<int> sched_jobs, sched_order;
   DevBuf<int> aca_counters;     // per-class job counters (reset before every chunk)
   DevBuf<double> aca_big_scratch;  // window scratch of the big-block ACA kernel (grown once)
+  DevBuf<int> aca_fallback;     // smooth-path kernels: blocks handed to the window kernels
   DevBuf<unsigned long long> aca_rej;  // [0] rejected columns, [1] their entries: current factorisation
   bool keff_known = false;      // k_eff holds the ranks of a complete factorisation of the own leaves
   bool phase_events = false;      // record ev_ph around the product phases (hm_mvp)
