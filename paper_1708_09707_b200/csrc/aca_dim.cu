@@ -23,8 +23,31 @@ static void classes_kind(const AcaClassLaunch& L, cudaStream_t s) {
   const int kmax = L.J[0].kmax;
   const int sms = L.sms;
   if (kmax <= 16) {
-    launch_cluster<DIM, KIND, 16, 4>(L.J[kAcaCl4], E, sms, s);
-    launch_cluster<DIM, KIND, 16, 8>(L.J[kAcaCl8], E, sms, s);
+    bool done = false;
+    if constexpr (DIM > 0) {
+      if (L.smooth) {
+        // smooth-path cluster kernels, then the general cluster kernels on their fallbacks
+        auto two_pass = [&](auto clc, int q) {
+          constexpr int CLq = decltype(clc)::value;
+          AcaJob Js = L.J[q];
+          Js.fb_list = L.fb_list + L.first[q];
+          Js.fb_count = L.fb_count + q;
+          launch_smooth_cluster<DIM, KIND, CLq>(Js, E, sms, s);
+          AcaJob Jw = L.J[q];
+          Jw.order = Js.fb_list;
+          Jw.njobs_dev = Js.fb_count;
+          Jw.counter = L.fb_counter + q;
+          launch_cluster<DIM, KIND, 16, CLq>(Jw, E, sms, s);
+        };
+        two_pass(std::integral_constant<int, 4>{}, kAcaCl4);
+        two_pass(std::integral_constant<int, 8>{}, kAcaCl8);
+        done = true;
+      }
+    }
+    if (!done) {
+      launch_cluster<DIM, KIND, 16, 4>(L.J[kAcaCl4], E, sms, s);
+      launch_cluster<DIM, KIND, 16, 8>(L.J[kAcaCl8], E, sms, s);
+    }
   } else {
     launch_cluster<DIM, KIND, 32, 4>(L.J[kAcaCl4], E, sms, s);
     launch_cluster<DIM, KIND, 32, 8>(L.J[kAcaCl8], E, sms, s);
@@ -36,10 +59,37 @@ static void classes_kind(const AcaClassLaunch& L, cudaStream_t s) {
     tr.mark("big (>4096)", s);
   }
   if (kmax <= 16) {
-    launch_win<DIM, KIND, 16, 16, 8, true>(L.J[4], E, sms, s);
-    tr.mark("win NW=16 (<=1024)", s);
-    launch_win<DIM, KIND, 8, 16, 8, true, 2>(L.J[3], E, sms, s);
-    tr.mark("NW=8 (<=512)", s);
+    bool mid_done = false;
+    if constexpr (DIM > 0) {
+      if (L.smooth) {
+        // <= 512 and <= 1024: the smooth cluster kernel on 1 and 2 CTAs (512 rows each),
+        // the window kernels on the blocks it hands back
+        auto two_pass = [&](auto clc, int q) {
+          constexpr int CLq = decltype(clc)::value;
+          AcaJob Js = L.J[q];
+          Js.fb_list = L.fb_list + L.first[q];
+          Js.fb_count = L.fb_count + q;
+          launch_smooth_cluster<DIM, KIND, CLq>(Js, E, sms, s);
+          AcaJob Jw = L.J[q];
+          Jw.order = Js.fb_list;
+          Jw.njobs_dev = Js.fb_count;
+          Jw.counter = L.fb_counter + q;
+          if constexpr (CLq == 2) launch_win<DIM, KIND, 16, 16, 8, true>(Jw, E, sms, s);
+          else launch_win<DIM, KIND, 8, 16, 8, true, 2>(Jw, E, sms, s);
+        };
+        two_pass(std::integral_constant<int, 2>{}, 4);
+        tr.mark("smooth CL=2 (<=1024)", s);
+        two_pass(std::integral_constant<int, 1>{}, 3);
+        tr.mark("smooth CL=1 (<=512)", s);
+        mid_done = true;
+      }
+    }
+    if (!mid_done) {
+      launch_win<DIM, KIND, 16, 16, 8, true>(L.J[4], E, sms, s);
+      tr.mark("win NW=16 (<=1024)", s);
+      launch_win<DIM, KIND, 8, 16, 8, true, 2>(L.J[3], E, sms, s);
+      tr.mark("NW=8 (<=512)", s);
+    }
     if constexpr (DIM > 0) {
       if (L.smooth) {
         // smooth-path kernels, then the general window kernel over the blocks they handed back
@@ -48,7 +98,8 @@ static void classes_kind(const AcaClassLaunch& L, cudaStream_t s) {
           AcaJob Js = L.J[q];
           Js.fb_list = L.fb_list + L.first[q];
           Js.fb_count = L.fb_count + q;
-          launch_smooth<DIM, KIND, NWq>(Js, E, sms, s);
+          if (L.smooth_pre) launch_smooth<DIM, KIND, NWq, true>(Js, E, sms, s);
+          else launch_smooth<DIM, KIND, NWq, false>(Js, E, sms, s);
           AcaJob Jw = L.J[q];
           Jw.order = Js.fb_list;
           Jw.njobs_dev = Js.fb_count;

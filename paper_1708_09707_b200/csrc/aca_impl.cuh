@@ -934,12 +934,15 @@ void launch_win(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, cudaS
 // If a candidate column is not qualified (a rejection: noise floor, zero column) the
 // block is handed to the general window kernel through a fallback list and recomputed
 // there from scratch, so every block's factors are bitwise the reference's either way.
-template <int NW>
+// PRE: the k raw candidate columns are evaluated up front into shared memory (more
+// shared memory per team, fewer teams per SM) or each rank's column is evaluated in place.
+template <int NW, bool PRE>
 __host__ __device__ constexpr size_t smooth_stride() {
-  return static_cast<size_t>(16) * (NW * 64 + 1) + static_cast<size_t>(16) * NW * 64 + 16 + 4 + 4 * NW + 8;
+  return (PRE ? static_cast<size_t>(16) * (NW * 64 + 1) : static_cast<size_t>(NW * 64 + 1)) +
+         static_cast<size_t>(2) * 16 * NW * 64 + 4 + 4 * NW + 8;
 }
 
-template <int DIM, int KIND, int NW>
+template <int DIM, int KIND, int NW, bool PRE>
 __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntry<DIM, KIND> E, int teams_per_cta) {
   constexpr int KC = 16;
   constexpr int TT = NW * 32, NCAP = 2 * TT, CS = NCAP + 1;
@@ -947,11 +950,11 @@ __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntr
   extern __shared__ double smem[];
   const int team = threadIdx.x / TT, t = threadIdx.x % TT, lane = t & 31, wib = t >> 5;
   if (team >= teams_per_cta) return;
-  double* base = smem + static_cast<size_t>(team) * smooth_stride<NW>();
-  double* s_col = base;                 // KC x CS: raw candidate columns A(i, c)
-  double* s_v = s_col + KC * CS;        // KC x NCAP: v_l[j]
-  double* s_up = s_v + KC * NCAP;       // KC: u_l[p]
-  double* s_yp = s_up + KC;             // the pivot row's point
+  double* base = smem + static_cast<size_t>(team) * smooth_stride<NW, PRE>();
+  double* s_col = base;                 // PRE: KC x CS raw candidate columns A(i, c); else 1 x CS scratch
+  double* s_v = s_col + (PRE ? KC : 1) * CS;  // KC x NCAP: v_l[j]
+  double* s_u = s_v + KC * NCAP;        // KC x NCAP: u_l[i] (no dynamic register indexing)
+  double* s_yp = s_u + KC * NCAP;       // the pivot row's point
   double* s_red = s_yp + 4;             // NW x 4: per-warp sum, nz, bv, bi
   double* s_misc = s_red + 4 * NW;      // [0] job [1] pivot value [2] exact verdict [3] scale
   const double kEps0sq = 1e-14 * 1e-14;
@@ -974,7 +977,7 @@ __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntr
     }
     // raw candidate columns 0 .. min(k, n) - 1, two columns (four entries) at a time
     const int ncol = min(kmax, n);
-    for (int c = 0; c < ncol; c += 2) {
+    for (int c = 0; PRE && c < ncol; c += 2) {
       const int c1 = c + 1 < ncol ? c + 1 : c;
       double a0, a1, b0, b1;
       E.eval2(y0, y1, cl + c, a0, a1);
@@ -985,9 +988,6 @@ __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntr
       s_col[c1 * CS + t + TT] = b1;
     }
     team_sync<NW>(team);
-    double uR0[KC], uR1[KC];
-#pragma unroll
-    for (int l = 0; l < KC; ++l) uR0[l] = uR1[l] = 0.0;
     bool used0 = false, used1 = false;
     double s_lo = 0.0, s_hi = 0.0, scale = 0.0;
     bool scale_exact = false;
@@ -997,8 +997,15 @@ __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntr
     for (int r = 0; r < kmax; ++r) {
       if (r >= n) break;  // no candidate column left: converged (aca.cpp:442-443)
       // column r residual (aca.cpp:363-364), rows of this thread
-      double a0 = s_col[r * CS + t], a1 = rv1 ? s_col[r * CS + t + TT] : 0.0;
-      SmoothChain<KC>::col2<NCAP>(a0, a1, uR0, uR1, r, s_v + r);
+      double a0, a1;
+      if constexpr (PRE) {
+        a0 = s_col[r * CS + t];
+        a1 = rv1 ? s_col[r * CS + t + TT] : 0.0;
+      } else {
+        E.eval2(y0, y1, cl + r, a0, a1);
+        if (!rv1) a1 = 0.0;
+      }
+      SmoothChain<KC>::col2s<NCAP>(a0, a1, s_u + t, s_u + t + TT, r, s_v + r);
       // fused reduction: norm2 (any order, bounded), nonzero flag, argmax over unused rows
       double sum = 0.0, bv = -1.0;
       int nz = 0, bi = 0x7fffffff;
@@ -1056,18 +1063,34 @@ __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntr
         }
       }
       if (st == 2) {  // inside the bound: the reference's sequential left folds
-        if (rv0) s_col[r * CS + t] = a0;  // raw column r is no longer needed
-        if (rv1) s_col[r * CS + t + TT] = a1;
-        team_sync<NW>(team);
-        if (t == 0) {
-          if (!scale_exact) {  // scale2 = left fold of the first accepted column, A(:, 0)
-            double f = hmul(s_col[0], s_col[0]);
-            for (int i = 1; i < m; ++i) f = hadd(f, hmul(s_col[i], s_col[i]));
+        double* sr = s_col + (PRE ? r * CS : 0);
+        if (!scale_exact) {
+          // scale2 = left fold of the first accepted column, A(:, 0) (raw: no cross yet)
+          double c0, c1;
+          if constexpr (PRE) {
+            c0 = s_col[t];
+            c1 = s_col[t + TT];
+          } else {
+            E.eval2(y0, y1, cl, c0, c1);
+          }
+          team_sync<NW>(team);
+          if (rv0) sr[t] = c0;
+          if (rv1) sr[t + TT] = c1;
+          team_sync<NW>(team);
+          if (t == 0) {
+            double f = hmul(sr[0], sr[0]);
+            for (int i = 1; i < m; ++i) f = hadd(f, hmul(sr[i], sr[i]));
             s_misc[3] = f;
           }
+          team_sync<NW>(team);
+        }
+        if (rv0) sr[t] = a0;  // raw column r is no longer needed
+        if (rv1) sr[t + TT] = a1;
+        team_sync<NW>(team);
+        if (t == 0) {
           const double sc = scale_exact ? scale : s_misc[3];
-          double f = hmul(s_col[r * CS], s_col[r * CS]);
-          for (int i = 1; i < m; ++i) f = hadd(f, hmul(s_col[r * CS + i], s_col[r * CS + i]));
+          double f = hmul(sr[0], sr[0]);
+          for (int i = 1; i < m; ++i) f = hadd(f, hmul(sr[i], sr[i]));
           s_misc[2] = f > hmul(kEps0sq, sc) ? 1.0 : 0.0;
         }
         team_sync<NW>(team);
@@ -1087,12 +1110,9 @@ __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntr
         s_hi = hmul(sum, 1.0 + 4.0 * gm);
       }
       const int p = bi;
-      // the pivot row's owner exports u_l[p], the pivot value and its point
+      // the pivot row's owner exports the pivot value and its point (u_l[p] is s_u[l][p])
       if (t == (p % TT)) {
         const bool q1 = p >= TT;
-#pragma unroll
-        for (int l = 0; l < KC; ++l)
-          if (l < r) s_up[l] = q1 ? uR1[l] : uR0[l];
         s_misc[1] = q1 ? a1 : a0;
 #pragma unroll
         for (int a = 0; a < DIM; ++a) s_yp[a] = q1 ? y1[a] : y0[a];
@@ -1101,8 +1121,8 @@ __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntr
       }
       team_sync<NW>(team);
       const PivotDiv pdiv(s_misc[1]);
-      SmoothChain<KC>::put(uR0, r, rv0 ? pdiv(a0) : 0.0);  // u_r = u_hat / pivot (aca.cpp:466-470)
-      SmoothChain<KC>::put(uR1, r, rv1 ? pdiv(a1) : 0.0);
+      s_u[r * NCAP + t] = rv0 ? pdiv(a0) : 0.0;  // u_r = u_hat / pivot (aca.cpp:466-470)
+      s_u[r * NCAP + t + TT] = rv1 ? pdiv(a1) : 0.0;
       // pivot row: v_r[j] = A(p, j) - sum_l u_l[p] v_l[j] (aca.cpp:474-481), columns t, t + TT
       {
         double yp[DIM];
@@ -1112,7 +1132,7 @@ __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntr
         const bool cv0 = j0 < n, cv1 = j1 < n;
         double b0, b1;
         E.eval2c(yp, cl + (cv0 ? j0 : 0), cl + (cv1 ? j1 : 0), b0, b1);
-        SmoothChain<KC>::row2<NCAP>(b0, b1, s_up, s_v + j0, s_v + j1, r);
+        SmoothChain<KC>::row2<NCAP, NCAP>(b0, b1, s_u + p, s_v + j0, s_v + j1, r);
         if (cv0) s_v[r * NCAP + j0] = b0;
         if (cv1) s_v[r * NCAP + j1] = b1;
       }
@@ -1138,8 +1158,8 @@ __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntr
     };
 #pragma unroll
     for (int l = 0; l < KC; ++l) {
-      if (rv0) U[uix(l, t)] = l < k_eff ? uR0[l] : 0.0;
-      if (rv1) U[uix(l, t + TT)] = l < k_eff ? uR1[l] : 0.0;
+      if (rv0) U[uix(l, t)] = l < k_eff ? s_u[l * NCAP + t] : 0.0;
+      if (rv1) U[uix(l, t + TT)] = l < k_eff ? s_u[l * NCAP + t + TT] : 0.0;
     }
     for (int idx = t; idx < n * KC; idx += TT) {
       const int j = idx >> 4, l = idx & 15;
@@ -1161,12 +1181,12 @@ __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntr
   }
 }
 
-template <int DIM, int KIND, int NW>
+template <int DIM, int KIND, int NW, bool PRE>
 void launch_smooth(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, cudaStream_t s) {
   if (J.njobs <= 0) return;
   constexpr int teams = 4 / NW;
-  const size_t smem = teams * smooth_stride<NW>() * sizeof(double);
-  auto kfn = aca_smooth_kernel<DIM, KIND, NW>;
+  const size_t smem = teams * smooth_stride<NW, PRE>() * sizeof(double);
+  auto kfn = aca_smooth_kernel<DIM, KIND, NW, PRE>;
   HM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int occ = 0;
   HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 128, smem));
@@ -1578,7 +1598,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
     cluster.sync();
     const long long job = static_cast<long long>(*rem(s_misc, 0));
     cluster.sync();  // everyone has read the job before rank 0 may overwrite it
-    if (job >= J.njobs) return;
+    if (job >= (J.njobs_dev ? static_cast<long long>(*J.njobs_dev) : J.njobs)) return;
     const int b = J.order[job];
     const int rl = J.rl[b], m = J.m[b], cl = J.cl[b], n = J.nn[b];
     double* U = J.U + (J.u_off[b] - J.u_base);
@@ -1942,6 +1962,245 @@ void launch_cluster(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, c
   HM_LAUNCH_CHECK();
 }
 
+// ---------------------------------------------------------------------------
+// Smooth-path cluster kernel (1024 < max(m, n) <= 512 CL, k = 16): the smooth_kernel
+// schedule over a thread-block cluster of CL CTAs, with ONE cluster barrier per rank.
+// CTA c owns rows [512c, 512c + 512) (two per thread, u_l of its rows in its shared
+// memory) and the row pass's columns [512c, 512c + 512); every CTA also keeps its own
+// copy of v_l at the k candidate columns (computed redundantly), so the column chain
+// never leaves the CTA.  Per rank each CTA publishes its partial (norm2, nonzero, argmax)
+// and its rows' residuals; after the barrier every CTA combines the CL partials in rank
+// order (identical decisions everywhere), reads the pivot value and u_l[p] from the
+// owner through distributed shared memory, and runs its row pass.  Published buffers
+// alternate by rank parity: a CTA rewrites a buffer only after the NEXT barrier, which
+// every reader of its previous contents has passed.  A rejection or a decision inside the
+// rigorous bound hands the block to the general cluster kernel (fallback list).
+template <int DIM, int KIND, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
+    aca_smooth_cluster_kernel(AcaJob J, KernelEntry<DIM, KIND> E) {
+  namespace cg = cooperative_groups;
+  constexpr int KC = 16, TT = 256, NCAP = 512;
+  static_assert(DIM > 0, "smooth cluster kernel: compile-time dimension");
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cr = static_cast<int>(cluster.block_rank());
+  extern __shared__ double smem[];
+  double* s_u = smem;                     // KC x NCAP: u_l of the own rows
+  double* s_res = s_u + KC * NCAP;        // 2 x NCAP: residuals of the own rows (rank parity)
+  double* s_vc = s_res + 2 * NCAP;        // KC x KC: v_l at the candidate columns
+  double* s_part = s_vc + KC * KC;        // 2 x 4: CTA partial (rank parity)
+  double* s_red = s_part + 8;             // 8 warps x 4
+  double* s_up = s_red + 32;              // KC: u_l[p]
+  double* s_misc = s_up + KC;             // [0] job
+  const int t = threadIdx.x, lane = t & 31, wib = t >> 5;
+  const double kEps0sq = 1e-14 * 1e-14;
+  const int kmax = J.kmax;
+  auto rem = [&](double* p, int rank) -> const double* { return cluster.map_shared_rank(p, rank); };
+
+  for (;;) {
+    if (cr == 0 && t == 0) s_misc[0] = static_cast<double>(atomicAdd(J.counter, 1));
+    cluster.sync();
+    const long long job = static_cast<long long>(*rem(s_misc, 0));
+    cluster.sync();
+    if (job >= J.njobs) return;
+    const int b = J.order[job];
+    const int rl = J.rl[b], m = J.m[b], cl = J.cl[b], n = J.nn[b];
+    const int row0 = cr * NCAP;
+    const int i0 = row0 + t, i1 = row0 + t + TT;
+    const bool rv0 = i0 < m, rv1 = i1 < m;
+    double y0[DIM], y1[DIM];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      y0[a] = rv0 ? __ldg(E.coords + a * E.n + rl + i0) : 0.0;
+      y1[a] = rv1 ? __ldg(E.coords + a * E.n + rl + i1) : 0.0;
+    }
+    double* V = J.V + (J.v_off[b] - J.v_base);
+    bool used0 = false, used1 = false;
+    double s_lo = 0.0, s_hi = 0.0;
+    const double gm = static_cast<double>(m) * 1.2e-16;
+    int k_eff = 0;
+    bool fallback = false;
+    for (int r = 0; r < kmax; ++r) {
+      if (r >= n) break;
+      const int par = r & 1;
+      // column r residual of the own rows (candidate column r: no rejection so far)
+      double a0, a1;
+      E.eval2(y0, y1, cl + r, a0, a1);
+      SmoothChain<KC>::col2s<NCAP, KC>(a0, a1, s_u + t, s_u + t + TT, r, s_vc + r);
+      // publish the residuals (the pivot value is read from its owner after the barrier)
+      s_res[par * NCAP + t] = a0;
+      s_res[par * NCAP + t + TT] = a1;
+      double sum = 0.0, bv = -1.0;
+      int nz = 0, bi = 0x7fffffff;
+      if (rv0) {
+        sum = hmul(a0, a0);
+        if (!used0) {
+          nz |= fabs(a0) > 0.0 ? 1 : 0;
+          bv = fabs(a0);
+          bi = i0;
+        }
+      }
+      if (rv1) {
+        sum = hadd(sum, hmul(a1, a1));
+        if (!used1) {
+          nz |= fabs(a1) > 0.0 ? 1 : 0;
+          argmax_combine(bv, bi, fabs(a1), i1);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+        nz |= __shfl_xor_sync(0xffffffffu, nz, o);
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        argmax_combine(bv, bi, ov, oi);
+      }
+      if (lane == 0) {
+        s_red[4 * wib] = sum;
+        s_red[4 * wib + 1] = static_cast<double>(nz);
+        s_red[4 * wib + 2] = bv;
+        s_red[4 * wib + 3] = static_cast<double>(bi);
+      }
+      __syncthreads();
+      if (t == 0) {
+        double cs = s_red[0], cb = s_red[2];
+        int cn = static_cast<int>(s_red[1]), ci = static_cast<int>(s_red[3]);
+        for (int w = 1; w < TT / 32; ++w) {
+          cs = hadd(cs, s_red[4 * w]);
+          cn |= static_cast<int>(s_red[4 * w + 1]);
+          argmax_combine(cb, ci, s_red[4 * w + 2], static_cast<int>(s_red[4 * w + 3]));
+        }
+        s_part[4 * par] = cs;
+        s_part[4 * par + 1] = static_cast<double>(cn);
+        s_part[4 * par + 2] = cb;
+        s_part[4 * par + 3] = static_cast<double>(ci);
+      }
+      cluster.sync();  // the ONE barrier of the rank: partials and residuals published
+      // identical decision in every CTA: partials combined in rank order
+      {
+        double ps[CL][4];
+#pragma unroll
+        for (int c = 0; c < CL; ++c) {
+          const double* q = rem(s_part + 4 * par, c);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) ps[c][e] = q[e];
+        }
+        sum = ps[0][0];
+        nz = static_cast<int>(ps[0][1]);
+        bv = ps[0][2];
+        bi = static_cast<int>(ps[0][3]);
+#pragma unroll
+        for (int c = 1; c < CL; ++c) {
+          sum = hadd(sum, ps[c][0]);
+          nz |= static_cast<int>(ps[c][1]);
+          argmax_combine(bv, bi, ps[c][2], static_cast<int>(ps[c][3]));
+        }
+      }
+      int st = 0;
+      if (nz) {
+        if (r == 0) {
+          st = 1;
+        } else {
+          const double Tlo = hmul(kEps0sq, s_lo), Thi = hmul(kEps0sq, s_hi);
+          const double lo = hmul(sum, 1.0 - 4.0 * gm), hi = hmul(sum, 1.0 + 4.0 * gm);
+          st = lo > Thi ? 1 : (hi <= Tlo ? 0 : 2);
+        }
+      }
+      if (st != 1) {  // rejection, or a decision the bound cannot settle: general kernel
+        fallback = true;
+        break;
+      }
+      if (r == 0) {
+        s_lo = hmul(sum, 1.0 - 4.0 * gm);
+        s_hi = hmul(sum, 1.0 + 4.0 * gm);
+      }
+      const int p = bi, po = p / NCAP, pl = p - po * NCAP;
+      // u_l[p] (l < r) and the pivot value from the owner CTA
+      if (t < r) s_up[t] = *rem(s_u + t * NCAP + pl, po);
+      if (t == KC) s_misc[1] = *rem(s_res + par * NCAP + pl, po);
+      if (po == cr && t == (pl % TT)) {
+        if (pl >= TT) used1 = true;
+        else used0 = true;
+      }
+      __syncthreads();
+      const PivotDiv pdiv(s_misc[1]);
+      s_u[r * NCAP + t] = rv0 ? pdiv(a0) : 0.0;  // u_r (aca.cpp:466-470)
+      s_u[r * NCAP + t + TT] = rv1 ? pdiv(a1) : 0.0;
+      // pivot row: own columns [512 cr, 512 cr + 512), plus the candidate columns c < k
+      {
+        double yp[DIM];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) yp[a] = __ldg(E.coords + a * E.n + rl + p);
+        const int j0 = row0 + t, j1 = row0 + t + TT;
+        const bool cv0 = j0 < n, cv1 = j1 < n;
+        const int jj0 = cv0 ? j0 : 0, jj1 = cv1 ? j1 : 0;
+        double b0, b1;
+        E.eval2c(yp, cl + jj0, cl + jj1, b0, b1);
+        SmoothChain<KC>::row2<1>(b0, b1, s_up, V + static_cast<long long>(jj0) * kmax,
+                                 V + static_cast<long long>(jj1) * kmax, r);
+        if (cv0) V[static_cast<long long>(j0) * kmax + r] = b0;
+        if (cv1) V[static_cast<long long>(j1) * kmax + r] = b1;
+        if (t < KC && t < n) {  // v_r at candidate column t (this CTA's copy)
+          double c0, c1;
+          E.eval2c(yp, cl + t, cl + t, c0, c1);
+          SmoothChain<KC>::row2<KC>(c0, c1, s_up, s_vc + t, s_vc + t, r);
+          s_vc[r * KC + t] = c0;
+        }
+      }
+      if (cr == 0 && t == 0) {
+        J.row_piv[static_cast<long long>(b) * kmax + r] = p;
+        J.col_piv[static_cast<long long>(b) * kmax + r] = r;
+      }
+      k_eff = r + 1;
+      __syncthreads();
+    }
+    if (fallback) {
+      if (cr == 0 && t == 0) J.fb_list[atomicAdd(J.fb_count, 1)] = b;
+      cluster.sync();  // every CTA is done with this block's shared buffers
+      continue;
+    }
+    double* U = J.U + (J.u_off[b] - J.u_base);
+    const int tsh = J.tile_shift;
+    auto uix = [&](int l, int i) -> long long {
+      if (tsh < 0) return static_cast<long long>(l) * m + i;
+      return ((static_cast<long long>(i >> tsh) * kmax + l) << tsh) + (i & ((1 << tsh) - 1));
+    };
+#pragma unroll
+    for (int l = 0; l < KC; ++l) {
+      if (rv0) U[uix(l, i0)] = l < k_eff ? s_u[l * NCAP + t] : 0.0;
+      if (rv1) U[uix(l, i1)] = l < k_eff ? s_u[l * NCAP + t + TT] : 0.0;
+    }
+    if (k_eff < kmax)
+      for (int j = row0 + t; j < min(n, row0 + NCAP); j += TT)
+        for (int l = k_eff; l < kmax; ++l) V[static_cast<long long>(j) * kmax + l] = 0.0;
+    if (cr == 0) {
+      for (int l = k_eff + t; l < kmax; l += TT) {
+        J.row_piv[static_cast<long long>(b) * kmax + l] = -1;
+        J.col_piv[static_cast<long long>(b) * kmax + l] = -1;
+      }
+      if (t == 0) {
+        J.k_eff[b] = k_eff;
+        if (J.evals) {
+          atomicAdd(J.evals, static_cast<unsigned long long>(k_eff) * m);
+          atomicAdd(J.evals + 1, static_cast<unsigned long long>(k_eff) * n);
+          atomicAdd(J.evals + 2, 1ull);
+        }
+      }
+    }
+    cluster.sync();  // shared buffers free for the next block
+  }
+}
+
+template <int DIM, int KIND, int CL>
+void launch_smooth_cluster(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, cudaStream_t s) {
+  if (J.njobs <= 0) return;
+  const size_t smem = sizeof(double) * (16 * 512 + 2 * 512 + 16 * 16 + 8 + 32 + 16 + 8);
+  auto kfn = aca_smooth_cluster_kernel<DIM, KIND, CL>;
+  HM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const long long clusters = std::min<long long>(J.njobs, std::max(1, 2 * sms / CL));
+  kfn<<<static_cast<unsigned>(clusters * CL), 256, smem, s>>>(J, E);
+  HM_LAUNCH_CHECK();
+}
+
 template <int DIM, int KIND, int KC>
 void launch_big(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int max_rows, int sms, DevBuf<double>& scratch,
                 cudaStream_t s) {
@@ -1993,6 +2252,7 @@ struct AcaClassLaunch {
   DevBuf<double>* big_scratch = nullptr;  // persistent window scratch of the big-block kernel
   PhaseTrace* tr = nullptr;
   bool smooth = false;         // smooth-path kernels for the <= 256 classes (fallback lists)
+  bool smooth_pre = false;     // ... with the candidate columns evaluated up front
   int* fb_list = nullptr;      // per class q at offset first[q]: blocks handed back
   int* fb_count = nullptr;     // kAcaClasses counts
   int* fb_counter = nullptr;   // kAcaClasses job counters of the fallback passes
