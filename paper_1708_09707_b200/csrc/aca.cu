@@ -156,6 +156,8 @@ void compute_aca(HMatrix& h, const AcaChunk& c, cudaStream_t s) {
     L.smooth = (e ? std::atoi(e) != 0 : h.d >= 3) && h.cfg.k == 16 && h.d <= 4;
     const char* ep = std::getenv("HM_SMOOTH_PRE");
     L.smooth_pre = ep ? std::atoi(ep) != 0 : false;
+    const char* em = std::getenv("HM_SMOOTH_MID");
+    L.smooth_mid = em ? std::atoi(em) != 0 : false;
   }
   L.fb_list = h.aca_fallback.get();
   L.fb_count = h.aca_counters.get() + kAcaClasses;

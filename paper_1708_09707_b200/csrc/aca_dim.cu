@@ -61,7 +61,7 @@ static void classes_kind(const AcaClassLaunch& L, cudaStream_t s) {
   if (kmax <= 16) {
     bool mid_done = false;
     if constexpr (DIM > 0) {
-      if (L.smooth) {
+      if (L.smooth && L.smooth_mid) {
         // <= 512 and <= 1024: the smooth cluster kernel on 1 and 2 CTAs (512 rows each),
         // the window kernels on the blocks it hands back
         auto two_pass = [&](auto clc, int q) {

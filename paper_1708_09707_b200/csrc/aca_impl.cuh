@@ -1296,10 +1296,13 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
         for (int i0 = t; i0 < m; i0 += 2 * TT) {
           const int i1 = i0 + TT;
           const bool ok1 = i1 < m;
+          // u_l of the two rows: right-aligned for Chain<KC>, left-aligned (u_l at [l]) for
+          // the straight-line SmoothChain cases (k = 16), whose V loads can be issued together
+          constexpr bool kLeft = KC == 16;
           double uR[2][KC];
 #pragma unroll
           for (int j = 0; j < KC; ++j) {
-            const int l = j - (KC - r);
+            const int l = kLeft ? (j < r ? j : -1) : j - (KC - r);
             uR[0][j] = l >= 0 ? U[uix(l, i0)] : 0.0;
             uR[1][j] = (l >= 0 && ok1) ? U[uix(l, i1)] : 0.0;
           }
@@ -1311,7 +1314,8 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
             double a0, a1;
             E.eval2(y0, y1, cl + col, a0, a1);
             if (!ok1) a1 = 0.0;
-            Chain<KC>::run2(a0, a1, uR[0], uR[1], r, V + static_cast<long long>(col) * kmax + (r - KC), 1);
+            if constexpr (kLeft) SmoothChain<16>::col2<1>(a0, a1, uR[0], uR[1], r, V + static_cast<long long>(col) * kmax);
+            else Chain<KC>::run2(a0, a1, uR[0], uR[1], r, V + static_cast<long long>(col) * kmax + (r - KC), 1);
             double* dst = win + static_cast<long long>(col % W) * PS;
             dst[i0] = a0;
             if (ok1) dst[i1] = a1;
@@ -1466,14 +1470,6 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
         for (int l = 0; l < r; ++l) s_up[l] = U[uix(l, p)];
       __syncthreads();
       const PivotDiv pdiv(acol[p]);
-      for (int i = t; i < m; i += 4 * TT) {
-        double a[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) a[u] = i + u * TT < m ? acol[i + u * TT] : 0.0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (i + u * TT < m) U[uix(r, i + u * TT)] = pdiv(a[u]);
-      }
       ev_row += n;
       {
         double yp[YD];
@@ -1492,8 +1488,12 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
             a1 = win[static_cast<long long>(jj % W) * PS + p];
           } else {
             E.eval2c(yp, cl + j, cl + jj, a0, a1);
-            Chain<KC>::run2v(a0, a1, uP, r, V + static_cast<long long>(j) * kmax + (r - KC),
-                             V + static_cast<long long>(jj) * kmax + (r - KC), 1);
+            if constexpr (KC == 16)
+              SmoothChain<16>::row2<1>(a0, a1, s_up, V + static_cast<long long>(j) * kmax,
+                                       V + static_cast<long long>(jj) * kmax, r);
+            else
+              Chain<KC>::run2v(a0, a1, uP, r, V + static_cast<long long>(j) * kmax + (r - KC),
+                               V + static_cast<long long>(jj) * kmax + (r - KC), 1);
             if (in0) a0 = win[static_cast<long long>(j % W) * PS + p];
             if (in1) a1 = win[static_cast<long long>(jj % W) * PS + p];
           }
@@ -1504,17 +1504,20 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
       __syncthreads();
       if (t == 0) s_mask[p >> 5] |= 1u << (p & 31);
       {
-        // per row: u_r[i] once, the W window entries loaded together (the loop was a
-        // load-latency-bound chain of L2 round trips, one column at a time)
+        // u_r = u_hat / pivot (aca.cpp:466-470) fused with the window cross: per row the
+        // accepted column's entry and the W window entries are loaded together, u_r goes
+        // to U and straight into the window updates (no reload)
         double vr[W];
 #pragma unroll
         for (int co = 0; co < W; ++co) vr[co] = co < filled ? V[static_cast<long long>(next + co) * kmax + r] : 0.0;
         for (int i = t; i < m; i += TT) {
-          const double u = U[uix(r, i)];
+          const double ah = acol[i];
           double a[W];
 #pragma unroll
           for (int co = 0; co < W; ++co)
             a[co] = co < filled ? win[static_cast<long long>((next + co) % W) * PS + i] : 0.0;
+          const double u = pdiv(ah);
+          U[uix(r, i)] = u;
 #pragma unroll
           for (int co = 0; co < W; ++co)
             if (co < filled) win[static_cast<long long>((next + co) % W) * PS + i] = hsub(a[co], hmul(u, vr[co]));
@@ -2253,6 +2256,8 @@ struct AcaClassLaunch {
   PhaseTrace* tr = nullptr;
   bool smooth = false;         // smooth-path kernels for the <= 256 classes (fallback lists)
   bool smooth_pre = false;     // ... with the candidate columns evaluated up front
+  bool smooth_mid = false;     // smooth cluster kernel also for <= 512 / <= 1024 (CL = 1, 2;
+                               // measured slower than the window kernels there: off)
   int* fb_list = nullptr;      // per class q at offset first[q]: blocks handed back
   int* fb_count = nullptr;     // kAcaClasses counts
   int* fb_counter = nullptr;   // kAcaClasses job counters of the fallback passes

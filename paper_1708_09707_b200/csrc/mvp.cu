@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(S) near_pair_kernel(const __grid_constant__ CU
 // against x_sigma as it goes (leaf (tau, sigma)), and stores it to a padded tile from which
 // thread t then folds column t against x_tau (leaf (sigma, tau)): half the kernel
 // evaluations of the reference's two dense GEMVs, the same sequential sums.
-template <int DIM, int S>
+template <int DIM, int S, int KIND = -1>
 __global__ void __launch_bounds__(S) near_pair_rc_kernel(const int* __restrict__ list,
                                                          const int* __restrict__ mirror, long long cnt,
                                                          const int* __restrict__ rl, const int* __restrict__ cl,
@@ -459,17 +459,36 @@ __global__ void __launch_bounds__(S) near_pair_rc_kernel(const int* __restrict__
     sxt[tid] = xm[r0 + tid];
     __syncthreads();
     double y = 0.0;
-    for (int j = 0; j < S; ++j) {
-      double r2 = 0.0;
+    if constexpr (KIND >= 0 && DIM > 0) {
+      // two entries per step (phi_x2: overlapped exp / K1 chains), folded in column order
+      for (int j = 0; j < S; j += 2) {
+        double r2a = 0.0, r2b = 0.0;
 #pragma unroll
-      for (int a = 0; a < YD; ++a) {
-        if (a >= dd) break;
-        const double dx = hsub(yi[a], scol[a * S + j]);
-        r2 = hadd(r2, hmul(dx, dx));
+        for (int a = 0; a < DIM; ++a) {
+          const double dxa = hsub(yi[a], scol[a * S + j]), dxb = hsub(yi[a], scol[a * S + j + 1]);
+          r2a = hadd(r2a, hmul(dxa, dxa));
+          r2b = hadd(r2b, hmul(dxb, dxb));
+        }
+        double av, bv;
+        phi_x2<KIND>(kp, r2a, r2b, av, bv);
+        y = hadd(y, hmul(av, sxs[j]));
+        y = hadd(y, hmul(bv, sxs[j + 1]));
+        sB[j * PS + tid] = av;
+        sB[(j + 1) * PS + tid] = bv;
       }
-      const double av = phi_r2(kp, r2);
-      y = hadd(y, hmul(av, sxs[j]));
-      sB[j * PS + tid] = av;
+    } else {
+      for (int j = 0; j < S; ++j) {
+        double r2 = 0.0;
+#pragma unroll
+        for (int a = 0; a < YD; ++a) {
+          if (a >= dd) break;
+          const double dx = hsub(yi[a], scol[a * S + j]);
+          r2 = hadd(r2, hmul(dx, dx));
+        }
+        const double av = phi_r2(kp, r2);
+        y = hadd(y, hmul(av, sxs[j]));
+        sB[j * PS + tid] = av;
+      }
     }
     part[static_cast<long long>(L) * S + tid] = y;
     __syncthreads();
@@ -1260,10 +1279,15 @@ void launch_near_pairs_rc(HMatrix& h, cudaStream_t s) {
   int sms = 0;
   HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h.device));
   const unsigned grid = static_cast<unsigned>(std::min<long long>(std::max(h.n_pairs, 1ll), sms * 16ll));
-#define HM_PRC(D)                                                                                               \
-  near_pair_rc_kernel<D, S><<<grid, S, 0, s>>>(h.pair_leaf.get(), h.pair_mirror.get(), h.n_pairs,              \
-                                               h.dense.rl.get(), h.dense.cl.get(), h.coords.get(), h.n, h.d, \
-                                               h.kp, h.xm.get(), h.part.get())
+#define HM_PRC(D)                                                                                             \
+  if (h.kp.kind == kGaussian)                                                                                 \
+    near_pair_rc_kernel<D, S, 0><<<grid, S, 0, s>>>(h.pair_leaf.get(), h.pair_mirror.get(), h.n_pairs,        \
+                                                    h.dense.rl.get(), h.dense.cl.get(), h.coords.get(), h.n,  \
+                                                    h.d, h.kp, h.xm.get(), h.part.get());                     \
+  else                                                                                                        \
+    near_pair_rc_kernel<D, S, 1><<<grid, S, 0, s>>>(h.pair_leaf.get(), h.pair_mirror.get(), h.n_pairs,        \
+                                                    h.dense.rl.get(), h.dense.cl.get(), h.coords.get(), h.n,  \
+                                                    h.d, h.kp, h.xm.get(), h.part.get())
   switch (h.d) {
     case 1: HM_PRC(1); break;
     case 2: HM_PRC(2); break;
