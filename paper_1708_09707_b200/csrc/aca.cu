@@ -163,12 +163,25 @@ void compute_aca(HMatrix& h, const AcaChunk& c, cudaStream_t s) {
   L.fb_count = h.aca_counters.get() + kAcaClasses;
   L.fb_counter = h.aca_counters.get() + 2 * kAcaClasses;
   for (int q = 0; q <= kAcaClasses; ++q) L.first[q] = first[q];
+  // HM_ACA_2STREAM=1: cluster / big-block kernels on the auxiliary stream beside the window
+  // kernels (tails overlap).  Measured at config 3: 5.80 s vs 5.70 s per product on one
+  // stream (the co-resident kernels compete for the same SMs), so one stream by default.
+  const bool two = std::getenv("HM_ACA_2STREAM") != nullptr && !tr.on && h.aux != nullptr;
+  if (two) {
+    HM_CUDA(cudaEventRecord(h.ev_fork, s));
+    HM_CUDA(cudaStreamWaitEvent(h.aux, h.ev_fork, 0));
+    L.s2 = h.aux;
+  }
   switch (h.d) {
     case 1: aca_classes_d1(L, s); break;
     case 2: aca_classes_d2(L, s); break;
     case 3: aca_classes_d3(L, s); break;
     case 4: aca_classes_d4(L, s); break;
     default: aca_classes_d0(L, s); break;
+  }
+  if (two) {
+    HM_CUDA(cudaEventRecord(h.ev_join, h.aux));
+    HM_CUDA(cudaStreamWaitEvent(s, h.ev_join, 0));
   }
   if (tr.on) {
     std::fprintf(stderr, "[hm_trace] aca classes: %lld %lld %lld %lld %lld | cl4 %lld cl8 %lld big %lld cta %lld\n",

@@ -17,11 +17,14 @@ namespace hmb {
 namespace aca_detail {
 
 template <int DIM, int KIND>
-static void classes_kind(const AcaClassLaunch& L, cudaStream_t s) {
+static void classes_kind(const AcaClassLaunch& L, cudaStream_t s0) {
   KernelEntry<DIM, KIND> E{L.coords, L.n, L.d, L.kp};
   PhaseTrace& tr = *L.tr;
   const int kmax = L.J[0].kmax;
   const int sms = L.sms;
+  // the size classes are independent: the cluster and big-block kernels go to a second
+  // stream so their tails overlap the window kernels (and vice versa)
+  cudaStream_t s = L.s2 ? L.s2 : s0;
   if (kmax <= 16) {
     bool done = false;
     if constexpr (DIM > 0) {
@@ -58,6 +61,7 @@ static void classes_kind(const AcaClassLaunch& L, cudaStream_t s) {
     else launch_big<DIM, KIND, 32>(L.J[kAcaBig], E, L.max_rows_big, sms, *L.big_scratch, s);
     tr.mark("big (>4096)", s);
   }
+  s = s0;
   if (kmax <= 16) {
     bool mid_done = false;
     if constexpr (DIM > 0) {

@@ -2262,6 +2262,7 @@ struct AcaClassLaunch {
   int* fb_count = nullptr;     // kAcaClasses counts
   int* fb_counter = nullptr;   // kAcaClasses job counters of the fallback passes
   long long first[kAcaClasses + 1] = {};
+  cudaStream_t s2 = nullptr;   // second stream: cluster / big kernels beside the window kernels
 };
 void aca_classes_d0(const AcaClassLaunch& L, cudaStream_t s);
 void aca_classes_d1(const AcaClassLaunch& L, cudaStream_t s);
