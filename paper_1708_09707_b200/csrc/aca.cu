@@ -3,6 +3,8 @@
 // instantiated per point dimension by aca_dim.cu.
 #include "aca_impl.cuh"
 
+#include <mutex>
+
 namespace hmb {
 using namespace aca_detail;
 
@@ -63,10 +65,20 @@ void plan_aca_chunk(HMatrix& h, AcaChunk& c, cudaStream_t s) {
     raise(kElogic, "plan_aca_chunk: schedule buffer too small");
   const bool eps = eps_live(h);
   const bool clus = std::getenv("HM_NO_CLUSTER") == nullptr;
-  for (long long b = c.c0; b < c.c1; ++b) {
-    const int q = aca_class(h.aca.h_m[b], h.aca.h_n[b], h.cfg.k, eps, clus);
-    ++c.ccount[q];
-    if (q == kAcaBig) c.max_rows_big = std::max(c.max_rows_big, h.aca.h_m[b]);
+  {
+    std::mutex mu;
+    parallel_blocks(c.c1 - c.c0, [&](long long b0, long long b1) {
+      long long cc[kAcaClasses] = {};
+      int mr = 0;
+      for (long long b = c.c0 + b0; b < c.c0 + b1; ++b) {
+        const int q = aca_class(h.aca.h_m[b], h.aca.h_n[b], h.cfg.k, eps, clus);
+        ++cc[q];
+        if (q == kAcaBig) mr = std::max(mr, h.aca.h_m[b]);
+      }
+      std::lock_guard<std::mutex> lk(mu);
+      for (int q = 0; q < kAcaClasses; ++q) c.ccount[q] += cc[q];
+      c.max_rows_big = std::max(c.max_rows_big, mr);
+    });
   }
   DevBuf<unsigned long long> keys;
   keys.alloc(cnt, s);

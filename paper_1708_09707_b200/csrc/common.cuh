@@ -2,7 +2,11 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <new>
+#include <thread>
+#include <vector>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -101,6 +105,52 @@ class DevBuf {
   cudaStream_t stream_ = nullptr;
   bool direct_ = false;
 };
+
+// Host mirrors of device arrays: page-locked storage (device-to-host copies at full link
+// rate) and default-initialising resize (no serial zero-fill of hundreds of MB).
+template <class T>
+struct PinnedAlloc {
+  using value_type = T;
+  PinnedAlloc() = default;
+  template <class U>
+  PinnedAlloc(const PinnedAlloc<U>&) {}
+  T* allocate(size_t n) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, n * sizeof(T)) != cudaSuccess) throw std::bad_alloc();
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, size_t) { cudaFreeHost(p); }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    if constexpr (sizeof...(A) == 0) ::new (static_cast<void*>(p)) U;  // default-init: no zeroing
+    else ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+  }
+  template <class U>
+  bool operator==(const PinnedAlloc<U>&) const { return true; }
+  template <class U>
+  bool operator!=(const PinnedAlloc<U>&) const { return false; }
+};
+template <class T>
+using HostVec = std::vector<T, PinnedAlloc<T>>;
+
+// f(begin, end) over [0, n) in contiguous blocks on up to `threads` host threads
+template <class F>
+void parallel_blocks(long long n, F&& f, int threads = 16) {
+  if (n <= 0) return;
+  const long long nt = std::max<long long>(1, std::min<long long>(threads, n / 65536 + 1));
+  if (nt == 1) {
+    f(0ll, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const long long per = (n + nt - 1) / nt;
+  for (long long t = 1; t < nt; ++t) {
+    const long long b = t * per, e = std::min(n, b + per);
+    if (b < e) pool.emplace_back([&f, b, e] { f(b, e); });
+  }
+  f(0ll, std::min(n, per));
+  for (auto& th : pool) th.join();
+}
 
 inline unsigned grid_for(long long n, int threads, long long cap = 1ll << 30) {
   long long g = (n + threads - 1) / threads;

@@ -1012,8 +1012,8 @@ hm_status hm_get_aca(hm_handle* H, int64_t* k_eff, int64_t* row_piv, int64_t* co
     cudaStream_t s = h.stream;
     const long long cnt = h.aca.count, kmax = h.cfg.k;
     if (h.cfg.world > 1) raise(kEinval, "hm_get_aca: single-rank handles only");
-    const std::vector<long long>& uo = h.h_uoff;
-    const std::vector<long long>& vo = h.h_voff;
+    const auto& uo = h.h_uoff;
+    const auto& vo = h.h_voff;
     std::vector<double> hu, hv;
     if (u || v) {
       hu.resize(uo[cnt]);

@@ -33,7 +33,7 @@ struct LeafList {
   DevBuf<unsigned char> depth;
   // per cluster slot: [start, end) of the run of leaves with that row cluster
   DevBuf<int> run_start, run_end;
-  std::vector<int> h_rl, h_m, h_cl, h_n;  // host mirrors (small; used for partitioning)
+  HostVec<int> h_rl, h_m, h_cl, h_n;  // host mirrors (chunk planning, partitioning, dumps)
 };
 
 // Per-kernel CUDA-event clock (enabled by hm_profile_begin): events are recorded on
@@ -131,7 +131,7 @@ struct HMatrix : HandleStreams {
   bool compact = false;  // stored factors with stride ke2 = k_eff rounded to even (mvp.cu compact_factors)
   DevBuf<int> k_eff, row_piv, col_piv;
   // host copies of the factor offsets (fixed at setup: the product never reads them back)
-  std::vector<long long> h_uoff, h_voff;
+  HostVec<long long> h_uoff, h_voff;
   // Factorisation schedule, fixed at setup.  The own admissible leaves are split into
   // chunks (recompute mode: the factor workspace holds one chunk; precompute: one chunk).
   // A chunk is a run of whole reference batches (partition_aca_queue, aca.cpp:229-250,

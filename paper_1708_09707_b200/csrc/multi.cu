@@ -398,7 +398,7 @@ void dispatch_rows_multi(const HMatrix& h, const MArgs& a, int near, bool far, c
   }
 }
 
-long long lower_bound_rows_m(const std::vector<int>& rl, long long v) {
+long long lower_bound_rows_m(const HostVec<int>& rl, long long v) {
   return std::lower_bound(rl.begin(), rl.end(), v, [](int x, long long y) { return x < y; }) - rl.begin();
 }
 

@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <chrono>
 #include <limits>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -722,7 +723,7 @@ void dispatch_rows(const HMatrix& h, const RowArgs& a, int near, bool far, cudaS
   }
 }
 
-long long lower_bound_rows(const std::vector<int>& rl, long long v) {
+long long lower_bound_rows(const HostVec<int>& rl, long long v) {
   return std::lower_bound(rl.begin(), rl.end(), v, [](int a, long long b) { return a < b; }) - rl.begin();
 }
 
@@ -1418,13 +1419,45 @@ void rank_sums(HMatrix& h, const int* ke, long long lo, long long hi) {
 // admissible leaves; in precompute mode also the factors themselves.
 void plan_far_field(HMatrix& h, cudaStream_t s) {
   const long long kmax = h.cfg.k;
-  std::vector<long long>& uo = h.h_uoff;
-  std::vector<long long>& vo = h.h_voff;
-  uo.assign(h.aca.count + 1, 0);
-  vo.assign(h.aca.count + 1, 0);
-  for (long long b = 0; b < h.aca.count; ++b) {
-    uo[b + 1] = uo[b] + kmax * h.aca.h_m[b];
-    vo[b + 1] = vo[b] + kmax * h.aca.h_n[b];
+  auto& uo = h.h_uoff;
+  auto& vo = h.h_voff;
+  uo.resize(h.aca.count + 1);
+  vo.resize(h.aca.count + 1);
+  {
+    // exclusive prefix sums of k*m and k*n over the admissible leaves: block sums on the
+    // host threads, then each block's running sum (two parallel passes)
+    const long long cnt = h.aca.count;
+    const int nb = 16;
+    std::vector<long long> bu(nb + 1, 0), bv(nb + 1, 0);
+    const long long per = (cnt + nb - 1) / nb;
+    parallel_blocks(nb, [&](long long b0, long long b1) {
+      for (long long q = b0; q < b1; ++q) {
+        long long su = 0, sv = 0;
+        for (long long b = q * per; b < std::min(cnt, (q + 1) * per); ++b) {
+          su += h.aca.h_m[b];
+          sv += h.aca.h_n[b];
+        }
+        bu[q + 1] = su;
+        bv[q + 1] = sv;
+      }
+    }, nb);
+    for (int q = 0; q < nb; ++q) {
+      bu[q + 1] += bu[q];
+      bv[q + 1] += bv[q];
+    }
+    parallel_blocks(nb, [&](long long b0, long long b1) {
+      for (long long q = b0; q < b1; ++q) {
+        long long su = bu[q] * kmax, sv = bv[q] * kmax;
+        for (long long b = q * per; b < std::min(cnt, (q + 1) * per); ++b) {
+          uo[b] = su;
+          vo[b] = sv;
+          su += kmax * h.aca.h_m[b];
+          sv += kmax * h.aca.h_n[b];
+        }
+      }
+    }, nb);
+    uo[cnt] = bu[nb] * kmax;
+    vo[cnt] = bv[nb] * kmax;
   }
   h.u_off.alloc(uo.size(), s);
   h.v_off.alloc(vo.size(), s);
@@ -1508,9 +1541,16 @@ void plan_far_field(HMatrix& h, cudaStream_t s) {
     c.ue = uo[c.c1];
     c.ve = vo[c.c1];
     c.row_lo = h.aca.h_rl[c.c0];
-    c.row_hi = 0;
-    for (long long b = c.c0; b < c.c1; ++b)
-      c.row_hi = std::max<long long>(c.row_hi, static_cast<long long>(h.aca.h_rl[b]) + h.aca.h_m[b]);
+    std::mutex mu;
+    long long row_hi = 0;
+    parallel_blocks(c.c1 - c.c0, [&](long long b0, long long b1) {
+      long long mx = 0;
+      for (long long b = c.c0 + b0; b < c.c0 + b1; ++b)
+        mx = std::max<long long>(mx, static_cast<long long>(h.aca.h_rl[b]) + h.aca.h_m[b]);
+      std::lock_guard<std::mutex> lk(mu);
+      row_hi = std::max(row_hi, mx);
+    });
+    c.row_hi = row_hi;
     plan_aca_chunk(h, c, s);
   }
   if (h.cfg.precompute_aca) {

@@ -6,6 +6,7 @@
 //   K3 box pyramid            tree.cpp:59-136        replaces per-level Alg. 7/8
 //   K4 traversal              tree.cpp:140-187       per-level classify + scan + emit
 //   K5 canonical order+split  tree.cpp:189-194, hmatrix.cpp:51-53
+#include <mutex>
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -623,13 +624,29 @@ void build_hmatrix(HMatrix& h, const double* coords_in) {
   build_spans(h, s);
   h.tm.tree_ms = ms_since(t1);
 
-  // algorithmic sizes
-  h.S_d = 0;
-  for (long long i = 0; i < h.dense.count; ++i) h.S_d += static_cast<double>(h.dense.h_m[i]) * h.dense.h_n[i];
-  h.sum_m_adm = h.sum_n_adm = 0;
-  for (long long i = 0; i < h.aca.count; ++i) {
-    h.sum_m_adm += h.aca.h_m[i];
-    h.sum_n_adm += h.aca.h_n[i];
+  // algorithmic sizes (host threads over the mirrors; integer partial sums, exact)
+  {
+    std::mutex mu;
+    long long sd = 0, sm = 0, sn = 0;
+    parallel_blocks(h.dense.count, [&](long long b0, long long b1) {
+      long long a = 0;
+      for (long long i = b0; i < b1; ++i) a += static_cast<long long>(h.dense.h_m[i]) * h.dense.h_n[i];
+      std::lock_guard<std::mutex> lk(mu);
+      sd += a;
+    });
+    parallel_blocks(h.aca.count, [&](long long b0, long long b1) {
+      long long a = 0, b = 0;
+      for (long long i = b0; i < b1; ++i) {
+        a += h.aca.h_m[i];
+        b += h.aca.h_n[i];
+      }
+      std::lock_guard<std::mutex> lk(mu);
+      sm += a;
+      sn += b;
+    });
+    h.S_d = static_cast<double>(sd);
+    h.sum_m_adm = static_cast<double>(sm);
+    h.sum_n_adm = static_cast<double>(sn);
   }
 
   // ---- row ownership: rank g owns the depth-log2(world) cluster g
@@ -652,10 +669,19 @@ void build_hmatrix(HMatrix& h, const double* coords_in) {
     h.row_begin = 0;
     h.row_end = n;
   }
-  h.S_d_own = 0;
-  for (long long i = 0; i < h.dense.count; ++i)
-    if (h.dense.h_rl[i] >= h.row_begin && h.dense.h_rl[i] < h.row_end)
-      h.S_d_own += static_cast<double>(h.dense.h_m[i]) * h.dense.h_n[i];
+  {
+    std::mutex mu;
+    long long own = 0;
+    parallel_blocks(h.dense.count, [&](long long b0, long long b1) {
+      long long a = 0;
+      for (long long i = b0; i < b1; ++i)
+        if (h.dense.h_rl[i] >= h.row_begin && h.dense.h_rl[i] < h.row_end)
+          a += static_cast<long long>(h.dense.h_m[i]) * h.dense.h_n[i];
+      std::lock_guard<std::mutex> lk(mu);
+      own += a;
+    });
+    h.S_d_own = static_cast<double>(own);
+  }
   h.tm.setup_ms = ms_since(t_setup);
 }
 
