@@ -149,6 +149,25 @@ struct KernelEntry {
       a1 = eval(y1, j);
     }
   }
+  // four entries: row y against points j0, j1 and rows z0, z1 against point jc
+  __device__ __forceinline__ void eval4(const double* y, long long j0, long long j1, const double* z0,
+                                        const double* z1, long long jc, double& a0, double& a1, double& c0,
+                                        double& c1) const {
+    if constexpr (KIND >= 0) {
+      const double r2[4] = {r2_of(y, j0), r2_of(y, j1), r2_of(z0, jc), r2_of(z1, jc)};
+      double f[4];
+      phi_xv<KIND, 4>(kp, r2, f);
+      a0 = f[0];
+      a1 = f[1];
+      c0 = f[2];
+      c1 = f[3];
+    } else {
+      a0 = eval(y, j0);
+      a1 = eval(y, j1);
+      c0 = eval(z0, jc);
+      c1 = eval(z1, jc);
+    }
+  }
   __device__ __forceinline__ void eval2c(const double* y, long long j0, long long j1, double& a0, double& a1) const {
     if constexpr (KIND >= 0) {
       phi_x2<KIND>(kp, r2_of(y, j0), r2_of(y, j1), a0, a1);

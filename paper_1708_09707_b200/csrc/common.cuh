@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <memory>
 #include <cstdint>
 #include <new>
 #include <thread>
@@ -106,32 +107,27 @@ class DevBuf {
   bool direct_ = false;
 };
 
-// Host mirrors of device arrays: page-locked storage (device-to-host copies at full link
-// rate) and default-initialising resize (no serial zero-fill of hundreds of MB).
+// Host mirrors of device arrays: default-initialising resize (no serial zero-fill of
+// hundreds of MB before the copy overwrites them).  Pageable on purpose: measured at
+// config-4 geometry, page-locking the 2-4 GB of mirrors costs more than it saves on the
+// device-to-host copies.
 template <class T>
-struct PinnedAlloc {
-  using value_type = T;
-  PinnedAlloc() = default;
+struct DefaultInitAlloc : std::allocator<T> {
   template <class U>
-  PinnedAlloc(const PinnedAlloc<U>&) {}
-  T* allocate(size_t n) {
-    void* p = nullptr;
-    if (cudaMallocHost(&p, n * sizeof(T)) != cudaSuccess) throw std::bad_alloc();
-    return static_cast<T*>(p);
-  }
-  void deallocate(T* p, size_t) { cudaFreeHost(p); }
+  struct rebind {
+    using other = DefaultInitAlloc<U>;
+  };
+  DefaultInitAlloc() = default;
+  template <class U>
+  DefaultInitAlloc(const DefaultInitAlloc<U>&) {}
   template <class U, class... A>
   void construct(U* p, A&&... a) {
     if constexpr (sizeof...(A) == 0) ::new (static_cast<void*>(p)) U;  // default-init: no zeroing
     else ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
   }
-  template <class U>
-  bool operator==(const PinnedAlloc<U>&) const { return true; }
-  template <class U>
-  bool operator!=(const PinnedAlloc<U>&) const { return false; }
 };
 template <class T>
-using HostVec = std::vector<T, PinnedAlloc<T>>;
+using HostVec = std::vector<T, DefaultInitAlloc<T>>;
 
 // f(begin, end) over [0, n) in contiguous blocks on up to `threads` host threads
 template <class F>

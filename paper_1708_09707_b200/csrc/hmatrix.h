@@ -201,6 +201,8 @@ void mvp_multi_morton(HMatrix& h, int R, int flags, cudaStream_t s);
 void morton_codes_device(const double* coords, long long n, int d, unsigned long long* codes, cudaStream_t s);
 // schedule of aca leaves [c0, c1) into h.sched_* at c.sched_off (setup time, may sync)
 void plan_aca_chunk(HMatrix& h, AcaChunk& c, cudaStream_t s);
+// every chunk of the own leaves [lo, hi) at once (false: not applicable, plan per chunk)
+bool plan_aca_chunks_all(HMatrix& h, long long lo, long long hi, cudaStream_t s);
 // factorise one planned chunk into h.U / h.V (offsets relative to c.ub / c.vb); no host sync
 void compute_aca(HMatrix& h, const AcaChunk& c, cudaStream_t s);
 // rejected-column counter of the current factorisation

@@ -247,6 +247,77 @@ __device__ __forceinline__ void bessel_k1_series_x2(double x0, double x1, double
   k1 = hsub(hadd(__drcp_rn(x1), hmul(l1, i11)), hmul(hmul(0.25, x1), sk1));
 }
 
+// V K1 series in one loop (V = 4: two pivot-row entries + two look-ahead column entries)
+template <int V>
+__device__ __forceinline__ void bessel_k1_series_xv(const double (&x)[V], double (&kv)[V]) {
+  double q[V], t[V], si[V], sk[V];
+  bool act[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    q[v] = hmul(hmul(0.25, x[v]), x[v]);
+    t[v] = 1.0;
+    si[v] = 0.0;
+    sk[v] = 0.0;
+    act[v] = true;
+  }
+  bool any = true;
+  for (int j = 0; j < 64 && any; ++j) {
+    const double psi = kK1Dev.psi[j], den = kK1Dev.den[j], rden = kK1Dev.rden[j];
+    any = false;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const double ni = hadd(si[v], t[v]);
+      const double nk = hadd(sk[v], hmul(psi, t[v]));
+      const double nx = div_by_const(hmul(t[v], q[v]), den, rden);
+      if (act[v]) {
+        si[v] = ni;
+        sk[v] = nk;
+        if (nx < hmul(1e-19, hadd(ni, 1.0))) act[v] = false;
+        else t[v] = nx;
+      }
+      any |= act[v];
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const double i1 = hmul(hmul(0.5, x[v]), si[v]);
+    const double h = hmul(0.5, x[v]);
+    double l = log_main(h);
+    if (!log_main_ok(h)) l = glibc_log(h);
+    kv[v] = hsub(hadd(__drcp_rn(x[v]), hmul(l, i1)), hmul(hmul(0.25, x[v]), sk[v]));
+  }
+}
+
+// phi for V squared distances at once (bitwise V scalar evaluations)
+template <int KIND, int V>
+__device__ __forceinline__ void phi_xv(const KernelParams& kp, const double (&r2)[V], double (&f)[V]) {
+  if constexpr (KIND == 0) {
+    double e[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) e[v] = exp_main(-r2[v]);
+#pragma unroll
+    for (int v = 0; v < V; ++v) f[v] = exp_main_ok(-r2[v]) ? e[v] : glibc_exp(-r2[v]);
+  } else {
+    double r[V];
+    bool series = true;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      r[v] = hm_sqrt(r2[v]);
+      series &= r[v] <= 2.0;
+    }
+    if (series) {
+      double kv[V];
+      bessel_k1_series_xv<V>(r, kv);
+#pragma unroll
+      for (int v = 0; v < V; ++v) f[v] = r2[v] == 0.0 ? kp.matern_norm : hmul(hmul(kv[v], r[v]), kp.matern_norm);
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        f[v] = r2[v] == 0.0 ? kp.matern_norm : hmul(hmul(bessel_k1(r[v]), r[v]), kp.matern_norm);
+    }
+  }
+}
+
 // phi for two squared distances (core.hpp:71-74, core.cpp:130-134); KIND 0 Gaussian, 1 Matern
 template <int KIND>
 __device__ __forceinline__ void phi_x2(const KernelParams& kp, double r2a, double r2b, double& fa, double& fb) {

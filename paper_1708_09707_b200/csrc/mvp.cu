@@ -1551,8 +1551,9 @@ void plan_far_field(HMatrix& h, cudaStream_t s) {
       row_hi = std::max(row_hi, mx);
     });
     c.row_hi = row_hi;
-    plan_aca_chunk(h, c, s);
   }
+  if (!plan_aca_chunks_all(h, lo, hi, s))
+    for (AcaChunk& c : h.chunks) plan_aca_chunk(h, c, s);
   if (h.cfg.precompute_aca) {
     const auto t0 = std::chrono::steady_clock::now();
     h.U.alloc(std::max(uo[hi] - uo[lo], 1ll), s);

@@ -1,0 +1,6 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_round2.py -m gpu -q -x -k "aca or mvp_matches or c1 or graph or invariant or timings" > gpurun_out/pytest_r2q.log 2>&1; tail -2 gpurun_out/pytest_r2q.log
+HM_SMOOTH=1 timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "aca or mvp_matches" > gpurun_out/pytest_r2q1.log 2>&1; tail -2 gpurun_out/pytest_r2q1.log
+HM_TRACE=1 timeout 900 python tools/trace_recompute.py 1048576 3 matern > gpurun_out/trace_m3_r2q.log 2>&1; grep -E "smooth|cluster|big \(|NW|'aca'" gpurun_out/trace_m3_r2q.log | tail -8
+HM_TRACE=1 timeout 900 python tools/trace_recompute.py 1048576 4 gaussian > gpurun_out/trace_g4_r2q.log 2>&1; grep -E "smooth|cluster|big \(|NW|'aca'" gpurun_out/trace_g4_r2q.log | tail -8
+timeout 900 python tools/setup_time.py 16777216 3 gaussian recompute 2 > gpurun_out/setup_c4_r2q.log 2>&1; tail -1 gpurun_out/setup_c4_r2q.log
