@@ -470,13 +470,14 @@ def run_ours(args):
 
     # end to end through the C ABI with host buffers (H2D + D2H inside)
     x_host = [symmetric(43 + t, n) for t in range(4)]
+    z_host = np.empty(n)  # the caller's result buffer, reused like a real solver loop would
     barrier()
     e2e_steps = max(3, args.steps // 2)
-    h.mvp(x_host[0])
+    h.mvp(x_host[0], out=z_host)
     barrier()
     te = time.perf_counter()
     for t in range(e2e_steps):
-        h.mvp(x_host[t % 4])
+        h.mvp(x_host[t % 4], out=z_host)
     barrier()
     e2e_s = (time.perf_counter() - te) / e2e_steps
     if world > 1:

@@ -253,11 +253,17 @@ class HMatrix:
         self.__del__()
 
     # --- products
-    def mvp(self, x, timings: Optional[MvpTimings] = None) -> np.ndarray:
+    def mvp(self, x, timings: Optional[MvpTimings] = None, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """z = H x (original ordering).  out: optional preallocated float64 result buffer."""
         x = np.ascontiguousarray(x, dtype=np.float64)
         if x.shape != (self.n,):
             raise InvalidArgument(HM_EINVAL, "mvp: vector length mismatch")
-        z = np.empty(self.n)
+        if out is not None:
+            if out.shape != (self.n,) or out.dtype != np.float64 or not out.flags["C_CONTIGUOUS"]:
+                raise InvalidArgument(HM_EINVAL, "mvp: out must be a contiguous float64 vector of length n")
+            z = out
+        else:
+            z = np.empty(self.n)
         t = _Timings()
         _check(_lib.hm_mvp(self._h, _ptr(x), _ptr(z), C.byref(t)))
         if timings is not None:
