@@ -469,8 +469,10 @@ def run_ours(args):
     launches_per_step = sum(c for (_, c) in prof.values()) / prof_steps
 
     # end to end through the C ABI with host buffers (H2D + D2H inside)
-    x_host = [symmetric(43 + t, n) for t in range(4)]
-    z_host = np.empty(n)  # the caller's result buffer, reused like a real solver loop would
+    # the caller's host buffers, page-locked (the e2e contract: inputs copied from pinned
+    # host memory), the result buffer reused like a solver loop would
+    x_host = [torch.from_numpy(symmetric(43 + t, n)).pin_memory().numpy() for t in range(4)]
+    z_host = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
     barrier()
     e2e_steps = max(3, args.steps // 2)
     h.mvp(x_host[0], out=z_host)

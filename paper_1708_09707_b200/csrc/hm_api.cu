@@ -167,6 +167,16 @@ hm_handle* new_handle(const hm_config* cfg, long long n, int d, int kernel, doub
   return H.release();
 }
 
+// host pointer in page-locked memory (DMA-able without staging)?
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 // dst <- src (host memory) with up to 4 threads over 1 MB chunks; after each chunk is in
 // place, on_chunk(offset, length) is called from the calling thread in order (used to
 // queue the chunk's DMA while later chunks are still being copied).
@@ -513,14 +523,21 @@ hm_status hm_mvp(hm_handle* H, const double* x, double* z, hm_timings* t) {
     if (h.zout.size() < static_cast<size_t>(h.n)) h.zout.alloc(h.n, s);
     // pinned staging: the copies run at full link rate (pageable copies are bounced
     // through a driver buffer at a fraction of it)
-    if (!H->pin_x) HM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&H->pin_x), bytes));
-    if (!H->pin_z) HM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&H->pin_z), bytes));
-    // x: host copies into the pinned staging run on a few threads, chunk by chunk, and each
-    // chunk's DMA is queued as soon as it is staged (copy and transfer overlap)
-    staged_copy(H->pin_x, x, bytes, [&](size_t off, size_t len) {
-      HM_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(h.xin.get()) + off, reinterpret_cast<char*>(H->pin_x) + off, len,
-                              cudaMemcpyHostToDevice, s));
-    });
+    if (!H->pin_x && !is_pinned(x)) HM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&H->pin_x), bytes));
+    if (!H->pin_z && !is_pinned(z)) HM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&H->pin_z), bytes));
+    // page-locked caller buffers (cudaHostAlloc / cudaHostRegister) are transferred
+    // directly; pageable ones go through the handle's pinned staging
+    const bool x_pinned = is_pinned(x), z_pinned = is_pinned(z);
+    if (x_pinned) {
+      HM_CUDA(cudaMemcpyAsync(h.xin.get(), x, bytes, cudaMemcpyHostToDevice, s));
+    } else {
+      // host copies into the pinned staging run on a few threads, chunk by chunk, and each
+      // chunk's DMA is queued as soon as it is staged (copy and transfer overlap)
+      staged_copy(H->pin_x, x, bytes, [&](size_t off, size_t len) {
+        HM_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(h.xin.get()) + off, reinterpret_cast<char*>(H->pin_x) + off,
+                                len, cudaMemcpyHostToDevice, s));
+      });
+    }
     h.phase_events = true;
     try {
       product(H, h.xin.get(), h.zout.get(), s);
@@ -529,9 +546,14 @@ hm_status hm_mvp(hm_handle* H, const double* x, double* z, hm_timings* t) {
       throw;
     }
     h.phase_events = false;
-    HM_CUDA(cudaMemcpyAsync(H->pin_z, h.zout.get(), bytes, cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaStreamSynchronize(s));
-    staged_copy(z, H->pin_z, bytes, nullptr);
+    if (z_pinned) {
+      HM_CUDA(cudaMemcpyAsync(z, h.zout.get(), bytes, cudaMemcpyDeviceToHost, s));
+      HM_CUDA(cudaStreamSynchronize(s));
+    } else {
+      HM_CUDA(cudaMemcpyAsync(H->pin_z, h.zout.get(), bytes, cudaMemcpyDeviceToHost, s));
+      HM_CUDA(cudaStreamSynchronize(s));
+      staged_copy(z, H->pin_z, bytes, nullptr);
+    }
     h.tm.mvp_ms = ms_since(t0);
     // MvpTimings (hmatrix.cpp:117-121): dense (near-field) and ACA (far-field) phases
     float dms = 0.f, ams = 0.f;
