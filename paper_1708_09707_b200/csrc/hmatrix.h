@@ -170,6 +170,7 @@ struct HMatrix : HandleStreams {
   DevBuf<double> xm, zm, xin, zout;
   // multi-RHS workspaces (multi.cu): rhs-major vectors, chunk-relative t, symmetric partials
   DevBuf<double> xmR, zmR, tR, partR, xinR, zoutR;
+  DevBuf<double> xmT;  // x interleaved [point][16] (the multi-RHS V^T x fold)
   DevBuf<long long> dmma_tiles;
   long long n_dmma_tiles = -1;  // -1: not built yet
   DevBuf<int> counter;

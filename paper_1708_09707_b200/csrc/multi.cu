@@ -30,12 +30,14 @@ namespace {
 constexpr int kMaxR = 16;
 
 __global__ void gather_multi_kernel(const double* __restrict__ X, long long ldx, const long long* __restrict__ perm,
-                                    long long n, int R, double* __restrict__ xm) {
+                                    long long n, int R, double* __restrict__ xm, double* __restrict__ xt) {
   const long long tot = n * R;
   for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < tot;
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long r = e / n, i = e - r * n;
-    xm[e] = X[r * ldx + perm[i]];  // permute_vector Forward (core.cpp:167-177)
+    const double v = X[r * ldx + perm[i]];  // permute_vector Forward (core.cpp:167-177)
+    xm[e] = v;
+    xt[i * kMaxR + r] = v;                  // interleaved copy: the R values of point i contiguous
   }
 }
 
@@ -57,7 +59,7 @@ __global__ void __launch_bounds__(256) t_multi_kernel(const int* __restrict__ or
                                                       const int* __restrict__ cl, const int* __restrict__ nn,
                                                       const int* __restrict__ k_eff,
                                                       const long long* __restrict__ v_off, long long v_base,
-                                                      const double* __restrict__ V, const double* __restrict__ xm,
+                                                      const double* __restrict__ V, const double* __restrict__ xt,
                                                       long long n_total, int kmax, int R, int G, long long t_base,
                                                       int* __restrict__ counter, double* __restrict__ t) {
   const int lane = threadIdx.x & 31, g = lane / G, l = lane % G;
@@ -75,18 +77,44 @@ __global__ void __launch_bounds__(256) t_multi_kernel(const int* __restrict__ or
       if (l >= ke) {
         for (int r = 0; r < R; ++r) tb[r] = 0.0;
       } else {
+        // x interleaved (xt[j * 16 + r]): the R values of column j are one 128-byte line,
+        // read as double2; v rows 4 columns ahead, so the loads of a group are in flight
+        // together (the folds stay sequential in j, aca.cpp:613-614)
         const double* v = V + (v_off[b] - v_base) + l;
-        const double* x = xm + cl[b];
+        const double2* x2 = reinterpret_cast<const double2*>(xt + static_cast<long long>(cl[b]) * kMaxR);
         double acc[RM];
-        const double v0 = v[0];
+        {
+          const double v0 = v[0];
 #pragma unroll
-        for (int r = 0; r < RM; ++r)
-          if (r < R) acc[r] = hmul(v0, x[r * n_total]);
-        for (int j = 1; j < n; ++j) {
+          for (int r2 = 0; r2 < RM / 2; ++r2) {
+            const double2 xv = __ldg(x2 + r2);
+            acc[2 * r2] = hmul(v0, xv.x);
+            acc[2 * r2 + 1] = hmul(v0, xv.y);
+          }
+        }
+        int j = 1;
+        for (; j + 4 <= n; j += 4) {
+          double vj[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) vj[u] = v[static_cast<long long>(j + u) * kmax];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+#pragma unroll
+            for (int r2 = 0; r2 < RM / 2; ++r2) {
+              const double2 xv = __ldg(x2 + static_cast<long long>(j + u) * (kMaxR / 2) + r2);
+              acc[2 * r2] = hadd(acc[2 * r2], hmul(vj[u], xv.x));
+              acc[2 * r2 + 1] = hadd(acc[2 * r2 + 1], hmul(vj[u], xv.y));
+            }
+          }
+        }
+        for (; j < n; ++j) {
           const double vj = v[static_cast<long long>(j) * kmax];
 #pragma unroll
-          for (int r = 0; r < RM; ++r)
-            if (r < R) acc[r] = hadd(acc[r], hmul(vj, x[r * n_total + j]));
+          for (int r2 = 0; r2 < RM / 2; ++r2) {
+            const double2 xv = __ldg(x2 + static_cast<long long>(j) * (kMaxR / 2) + r2);
+            acc[2 * r2] = hadd(acc[2 * r2], hmul(vj, xv.x));
+            acc[2 * r2 + 1] = hadd(acc[2 * r2 + 1], hmul(vj, xv.y));
+          }
         }
 #pragma unroll
         for (int r = 0; r < RM; ++r)
@@ -195,13 +223,37 @@ __global__ void __launch_bounds__(128) rows_multi_kernel(MArgs a) {
         const double* tl = a.t + (static_cast<long long>(L) - a.t_base) * kmax * R;
 #pragma unroll
         for (int r = 0; r < RM; ++r) y[r] = 0.0;
-        for (int l = 0; l < ke; ++l) {
-          const long long ui = tsh < 0 ? static_cast<long long>(l) * mb + ii
-                                       : (((ii >> tsh) * kmax + l) << tsh) + (ii & ((1ll << tsh) - 1));
-          const double uv = __ldcs(u + ui);
+        if (R == RM && kmax == 16 && RM % 2 == 0) {
+          // all u_l of the row issued at once (HBM latency paid once per leaf, not per rank);
+          // t_l as double2 (R values contiguous per rank)
+          double uv[16];
 #pragma unroll
-          for (int r = 0; r < RM; ++r)
-            if (r < R) y[r] = hadd(y[r], hmul(uv, __ldg(tl + l * R + r)));  // ((0 + u_0 t_0) + ...) aca.cpp:616
+          for (int l = 0; l < 16; ++l) {
+            const long long ui = tsh < 0 ? static_cast<long long>(l) * mb + ii
+                                         : (((ii >> tsh) * 16 + l) << tsh) + (ii & ((1ll << tsh) - 1));
+            uv[l] = l < ke ? __ldcs(u + ui) : 0.0;
+          }
+          const double2* t2 = reinterpret_cast<const double2*>(tl);
+#pragma unroll
+          for (int l = 0; l < 16; ++l) {
+            if (l < ke) {
+#pragma unroll
+              for (int r2 = 0; r2 < RM / 2; ++r2) {
+                const double2 tv = __ldg(t2 + l * (RM / 2) + r2);
+                y[2 * r2] = hadd(y[2 * r2], hmul(uv[l], tv.x));  // ((0 + u_0 t_0) + ...) aca.cpp:616
+                y[2 * r2 + 1] = hadd(y[2 * r2 + 1], hmul(uv[l], tv.y));
+              }
+            }
+          }
+        } else {
+          for (int l = 0; l < ke; ++l) {
+            const long long ui = tsh < 0 ? static_cast<long long>(l) * mb + ii
+                                         : (((ii >> tsh) * kmax + l) << tsh) + (ii & ((1ll << tsh) - 1));
+            const double uv = __ldcs(u + ui);
+#pragma unroll
+            for (int r = 0; r < RM; ++r)
+              if (r < R) y[r] = hadd(y[r], hmul(uv, __ldg(tl + l * R + r)));  // ((0 + u_0 t_0) + ...) aca.cpp:616
+          }
         }
 #pragma unroll
         for (int r = 0; r < RM; ++r)
@@ -449,7 +501,7 @@ void launch_t_multi(HMatrix& h, const int* order, long long njobs, long long v_b
   const unsigned grid = static_cast<unsigned>(std::min<long long>((njobs * G / 32 + 8) / 8 + 1, sms * 8ll));
 #define HM_T(RM)                                                                                                   \
   t_multi_kernel<RM><<<grid, 256, 0, s>>>(order, njobs, h.aca.cl.get(), h.aca.n.get(), h.k_eff.get(),              \
-                                          h.v_off.get(), v_base, h.V.get(), h.xmR.get(), h.n, kmax, R, G, t_base, \
+                                          h.v_off.get(), v_base, h.V.get(), h.xmT.get(), h.n, kmax, R, G, t_base, \
                                           h.counter.get(), h.tR.get())
   if (R <= 4) HM_T(4);
   else if (R <= 8) HM_T(8);
@@ -575,6 +627,10 @@ void mvp_multi_morton(HMatrix& h, int R, int flags, cudaStream_t s) {
 void ensure_multi(HMatrix& h, int R, cudaStream_t s) {
   const size_t nv = static_cast<size_t>(h.n) * R;
   if (h.xmR.size() < nv) h.xmR.alloc(nv, s);
+  if (h.xmT.size() < static_cast<size_t>(h.n) * kMaxR) {  // interleaved copy, padded to 16 per point
+    h.xmT.alloc(static_cast<size_t>(h.n) * kMaxR, s);
+    h.xmT.zero(s);
+  }
   if (h.zmR.size() < nv) h.zmR.alloc(nv, s);
   if (h.cfg.precompute_aca) {
     const size_t nt = static_cast<size_t>(std::max(h.aca.count, 1ll)) * h.cfg.k * R;
@@ -588,7 +644,8 @@ void ensure_multi(HMatrix& h, int R, cudaStream_t s) {
 }
 
 void gather_multi(HMatrix& h, const double* X, long long ldx, int R, cudaStream_t s) {
-  gather_multi_kernel<<<grid_for(h.n * R, 256, 1 << 16), 256, 0, s>>>(X, ldx, h.perm.get(), h.n, R, h.xmR.get());
+  gather_multi_kernel<<<grid_for(h.n * R, 256, 1 << 16), 256, 0, s>>>(X, ldx, h.perm.get(), h.n, R, h.xmR.get(),
+                                                                       h.xmT.get());
   HM_LAUNCH_CHECK();
 }
 
