@@ -141,6 +141,7 @@ struct HMatrix : HandleStreams {
   std::vector<AcaChunk> chunks;
   long long n_batches = 0;      // reference batches of the own admissible leaves
   DevBuf<int> sched_jobs, sched_order;
+  DevBuf<int> sched_corder;     // multi-RHS: per chunk, leaves by column start (x reuse in L2)
   DevBuf<int> aca_counters;     // per-class job counters (reset before every chunk)
   DevBuf<double> aca_big_scratch;  // window scratch of the big-block ACA kernel (grown once)
   DevBuf<int> aca_fallback;     // smooth-path kernels: blocks handed to the window kernels

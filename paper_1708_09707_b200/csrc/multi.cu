@@ -266,6 +266,83 @@ __global__ void __launch_bounds__(128) rows_multi_kernel(MArgs a) {
     if (r < R) a.zm[r * a.n + i] = z[r];
 }
 
+// Far field only, 16 right-hand sides: TWO threads per row, each owning 8 of them (the
+// register footprint of 16 accumulators + 16 leaf partials per thread held the one-thread-
+// per-row kernel to 8 warps per SM).  Per leaf the thread's u_l are issued 4 ranks ahead;
+// the folds are the reference's: y_r = ((0 + u_0 t_0r) + u_1 t_1r) + ..., z_r += y_r in
+// leaf order (aca.cpp:616, hmatrix.cpp:96-113) -- bitwise the one-thread version.
+__global__ void __launch_bounds__(128, 6) rows_multi_far16_kernel(MArgs a) {
+  constexpr int RH = 8;
+  const long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long i = a.row_begin + (g >> 1);
+  const int half = static_cast<int>(g & 1);
+  if (i >= a.row_end) return;
+  const int c = __ldg(a.row_cluster + i);
+  double z[RH];
+#pragma unroll
+  for (int r = 0; r < RH; ++r) z[r] = a.z_acc ? a.zm[(half * RH + r) * a.n + i] : 0.0;
+  const int tsh = a.tile_shift;
+  const int p1 = __ldg(a.aspan_ptr + c + 1);
+  for (int p = __ldg(a.aspan_ptr + c); p < p1; ++p) {
+    const int rs = static_cast<int>(max(static_cast<long long>(__ldg(a.aspans + 2 * p)), a.a_lo));
+    const int re = static_cast<int>(min(static_cast<long long>(__ldg(a.aspans + 2 * p + 1)), a.a_hi));
+    for (int L = rs; L < re; ++L) {
+      const int r0 = __ldg(a.a_rl + L), mb = __ldg(a.a_m + L), ke = __ldg(a.a_keff + L);
+      const double* u = a.U + (__ldg(a.a_uoff + L) - a.a_ubase);
+      const long long ii = i - r0;
+      auto uidx = [&](int l) -> long long {
+        return tsh < 0 ? static_cast<long long>(l) * mb + ii : (((ii >> tsh) * 16 + l) << tsh) + (ii & ((1ll << tsh) - 1));
+      };
+      const double2* t2 = reinterpret_cast<const double2*>(a.t + (static_cast<long long>(L) - a.t_base) * 16 * 16) +
+                          half * (RH / 2);
+      double y[RH];
+#pragma unroll
+      for (int r = 0; r < RH; ++r) y[r] = 0.0;
+      for (int l0 = 0; l0 < ke; l0 += 4) {
+        double uv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) uv[q] = l0 + q < ke ? __ldcs(u + uidx(l0 + q)) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (l0 + q < ke) {
+#pragma unroll
+            for (int r2 = 0; r2 < RH / 2; ++r2) {
+              const double2 tv = __ldg(t2 + (l0 + q) * 8 + r2);
+              y[2 * r2] = hadd(y[2 * r2], hmul(uv[q], tv.x));
+              y[2 * r2 + 1] = hadd(y[2 * r2 + 1], hmul(uv[q], tv.y));
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RH; ++r) z[r] = hadd(z[r], y[r]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RH; ++r) a.zm[(half * RH + r) * a.n + i] = z[r];
+}
+
+// Column-ordered fold schedule for the multi-RHS V^T X pass: per chunk its leaves sorted
+// by column cluster start, so the x segments (16 values per point, 128 B) of consecutive
+// leaves coincide and stay in L2.  Any order gives the same t (independent folds).
+__global__ void col_keys_kernel(const int* __restrict__ cl, long long lo, long long cnt,
+                                const long long* __restrict__ starts, int nchunks,
+                                unsigned long long* __restrict__ keys, unsigned* __restrict__ vals) {
+  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < cnt;
+       q += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long b = lo + q;
+    int a0 = 0, z = nchunks;
+    while (z - a0 > 1) {
+      const int mid = (a0 + z) >> 1;
+      if (starts[mid] <= b) a0 = mid;
+      else z = mid;
+    }
+    keys[q] = (static_cast<unsigned long long>(a0) << 54) | (static_cast<unsigned long long>(cl[b]) << 27) |
+              static_cast<unsigned long long>(b - starts[a0]);
+    vals[q] = static_cast<unsigned>(b);
+  }
+}
+
 // Symmetric stored near field, R right-hand sides: one CTA of S threads per stored
 // S x S block B, staged once into a padded shared tile; thread t folds row t of B
 // against x_sigma (leaf (tau, sigma)) and column t against x_tau (leaf (sigma, tau)),
@@ -441,6 +518,14 @@ void dispatch_rows_multi_r(const MArgs& a, int near, bool far, cudaStream_t s) {
 }
 
 void dispatch_rows_multi(const HMatrix& h, const MArgs& a, int near, bool far, cudaStream_t s) {
+  if (near == 0 && far && a.R == 16 && a.kmax == 16) {
+    const long long rows = a.row_end - a.row_begin;
+    if (rows > 0) {
+      rows_multi_far16_kernel<<<grid_for(2 * rows, 128), 128, 0, s>>>(a);
+      HM_LAUNCH_CHECK();
+    }
+    return;
+  }
   switch (h.d) {
     case 1: dispatch_rows_multi_r<1>(a, near, far, s); break;
     case 2: dispatch_rows_multi_r<2>(a, near, far, s); break;
@@ -562,7 +647,32 @@ void near_dmma(HMatrix& h, const MArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-// Morton-ordered product of R right-hand sides: h.xmR -> h.zmR (own rows).
+// the column-ordered schedule (built by the first multi-RHS product; falls back to the
+// size-ordered schedule when the packed key does not fit)
+static const int* multi_fold_order(HMatrix& h, long long lo, long long hi, cudaStream_t s) {
+  const long long cnt = hi - lo;
+  const int nch = static_cast<int>(h.chunks.size());
+  if (cnt <= 0 || nch == 0 || nch > 1000 || cnt >= (1ll << 27) || h.n >= (1ll << 27)) return h.sched_order.get();
+  if (h.sched_corder.size() < static_cast<size_t>(cnt)) {
+    std::vector<long long> starts(nch + 1);
+    for (int c = 0; c < nch; ++c) starts[c] = h.chunks[c].c0;
+    starts[nch] = h.chunks.back().c1;
+    DevBuf<long long> ds;
+    DevBuf<unsigned long long> keys;
+    ds.alloc(nch + 1, s);
+    keys.alloc(cnt, s);
+    h.sched_corder.alloc(cnt, s);
+    HM_CUDA(cudaMemcpyAsync(ds.get(), starts.data(), sizeof(long long) * (nch + 1), cudaMemcpyHostToDevice, s));
+    col_keys_kernel<<<grid_for(cnt, 256, 1 << 16), 256, 0, s>>>(h.aca.cl.get(), lo, cnt, ds.get(), nch, keys.get(),
+                                                                 reinterpret_cast<unsigned*>(h.sched_corder.get()));
+    HM_LAUNCH_CHECK();
+    radix_sort_pairs(keys.get(), reinterpret_cast<unsigned*>(h.sched_corder.get()), cnt, s);
+    HM_CUDA(cudaStreamSynchronize(s));  // the key buffers are released on return
+  }
+  return h.sched_corder.get();
+}
+
+// Morton-ordered product of R right-hand sides: h.xmR -> h.zmR (own rows).// Morton-ordered product of R right-hand sides: h.xmR -> h.zmR (own rows).
 void mvp_multi_morton(HMatrix& h, int R, int flags, cudaStream_t s) {
   if (R < 1 || R > kMaxR) raise(kEinval, "mvp_multi: 1 <= nrhs <= 16 per pass");
   const bool dmma = (flags & 1) != 0;
@@ -589,7 +699,7 @@ void mvp_multi_morton(HMatrix& h, int R, int flags, cudaStream_t s) {
     }
     const AcaChunk c0c = h.chunks.empty() ? AcaChunk{} : h.chunks.front();
     const long long ub = c0c.ub, vb = c0c.vb;
-    launch_t_multi(h, h.sched_order.get() + c0c.sched_off, ahi - alo, vb, 0, R, s);
+    launch_t_multi(h, multi_fold_order(h, alo, ahi, s) + c0c.sched_off, ahi - alo, vb, 0, R, s);
     a.a_ubase = ub;
     a.a_lo = alo;
     a.a_hi = ahi;
@@ -601,13 +711,14 @@ void mvp_multi_morton(HMatrix& h, int R, int flags, cudaStream_t s) {
   if (dmma) near_dmma(h, a, s);
   else dispatch_rows_multi(h, a, near, false, s);
   reset_aca_rejections(h, s);
+  const int* corder = multi_fold_order(h, alo, ahi, s);
   for (const AcaChunk& c : h.chunks) {
     const long long c0 = c.c0, c1 = c.c1;
     if (h.U.size() < static_cast<size_t>(c.ue - c.ub)) h.U.alloc(c.ue - c.ub, s);
     if (h.V.size() < static_cast<size_t>(c.ve - c.vb)) h.V.alloc(c.ve - c.vb, s);
     if (h.tR.size() < static_cast<size_t>((c1 - c0) * kmax * R)) h.tR.alloc((c1 - c0) * kmax * R, s);
     compute_aca(h, c, s);
-    launch_t_multi(h, h.sched_order.get() + c.sched_off, c1 - c0, c.vb, c0, R, s);
+    launch_t_multi(h, corder + c.sched_off, c1 - c0, c.vb, c0, R, s);
     MArgs b = base_margs(h, R);
     b.z_acc = 1;
     b.a_ubase = c.ub;

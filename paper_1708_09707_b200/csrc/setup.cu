@@ -7,6 +7,7 @@
 //   K4 traversal              tree.cpp:140-187       per-level classify + scan + emit
 //   K5 canonical order+split  tree.cpp:189-194, hmatrix.cpp:51-53
 #include <mutex>
+#include <cstring>
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -393,6 +394,46 @@ void build_spans(HMatrix& h, cudaStream_t s) {
   }
 }
 
+// Device array -> host mirror through a process-wide page-locked staging ring: each 32 MB
+// piece is DMA'd at full link rate and copied out by the host threads (which also take the
+// first-touch page faults of the fresh mirror in parallel), while the next piece is in
+// flight.  Small arrays copy directly.
+void mirror_to_host(int* dst, const int* src, long long cnt, cudaStream_t s) {
+  if (cnt <= 0) return;
+  const size_t bytes = sizeof(int) * static_cast<size_t>(cnt);
+  if (bytes < (size_t(8) << 20)) {
+    HM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  constexpr size_t kPiece = size_t(32) << 20;
+  static std::mutex mu;
+  static char* ring[2] = {nullptr, nullptr};
+  static cudaEvent_t done[2] = {nullptr, nullptr};
+  std::lock_guard<std::mutex> lk(mu);
+  for (int q = 0; q < 2; ++q) {
+    if (!ring[q]) HM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ring[q]), kPiece));
+    if (!done[q]) HM_CUDA(cudaEventCreateWithFlags(&done[q], cudaEventDisableTiming));
+  }
+  const size_t npieces = (bytes + kPiece - 1) / kPiece;
+  auto issue = [&](size_t p) {
+    const size_t off = p * kPiece, len = std::min(kPiece, bytes - off);
+    HM_CUDA(cudaMemcpyAsync(ring[p & 1], reinterpret_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost, s));
+    HM_CUDA(cudaEventRecord(done[p & 1], s));
+  };
+  issue(0);
+  for (size_t p = 0; p < npieces; ++p) {
+    if (p + 1 < npieces) issue(p + 1);
+    HM_CUDA(cudaEventSynchronize(done[p & 1]));
+    const size_t off = p * kPiece, len = std::min(kPiece, bytes - off);
+    const char* from = ring[p & 1];
+    char* to = reinterpret_cast<char*>(dst) + off;
+    parallel_blocks(static_cast<long long>(len), [&](long long b0, long long b1) {
+      std::memcpy(to + b0, from + b0, static_cast<size_t>(b1 - b0));
+    }, 8);
+  }
+}
+
 void alloc_list(LeafList& l, long long cnt, long long nslots, cudaStream_t s) {
   l.count = cnt;
   l.rl.alloc(cnt, s);
@@ -613,12 +654,10 @@ void build_hmatrix(HMatrix& h, const double* coords_in) {
     l->h_m.resize(l->count);
     l->h_cl.resize(l->count);
     l->h_n.resize(l->count);
-    if (l->count) {
-      HM_CUDA(cudaMemcpyAsync(l->h_rl.data(), l->rl.get(), sizeof(int) * l->count, cudaMemcpyDeviceToHost, s));
-      HM_CUDA(cudaMemcpyAsync(l->h_m.data(), l->m.get(), sizeof(int) * l->count, cudaMemcpyDeviceToHost, s));
-      HM_CUDA(cudaMemcpyAsync(l->h_cl.data(), l->cl.get(), sizeof(int) * l->count, cudaMemcpyDeviceToHost, s));
-      HM_CUDA(cudaMemcpyAsync(l->h_n.data(), l->n.get(), sizeof(int) * l->count, cudaMemcpyDeviceToHost, s));
-    }
+    mirror_to_host(l->h_rl.data(), l->rl.get(), l->count, s);
+    mirror_to_host(l->h_m.data(), l->m.get(), l->count, s);
+    mirror_to_host(l->h_cl.data(), l->cl.get(), l->count, s);
+    mirror_to_host(l->h_n.data(), l->n.get(), l->count, s);
   }
   HM_CUDA(cudaStreamSynchronize(s));
   build_spans(h, s);
