@@ -149,6 +149,24 @@ struct KernelEntry {
       a1 = eval(y1, j);
     }
   }
+  // r2 between two points held in registers / shared memory (no global loads)
+  __device__ __forceinline__ static double r2_pts(const double* y, const double* z) {
+    double r2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < (DIM > 0 ? DIM : 1); ++a) {
+      const double dx = hsub(y[a], z[a]);
+      r2 = hadd(r2, hmul(dx, dx));
+    }
+    return r2;
+  }
+  __device__ __forceinline__ void phi2(double r2a, double r2b, double& a0, double& a1) const {
+    if constexpr (KIND >= 0) {
+      phi_x2<KIND>(kp, r2a, r2b, a0, a1);
+    } else {
+      a0 = phi_r2(kp, r2a);
+      a1 = phi_r2(kp, r2b);
+    }
+  }
   // four entries: row y against points j0, j1 and rows z0, z1 against point jc
   __device__ __forceinline__ void eval4(const double* y, long long j0, long long j1, const double* z0,
                                         const double* z1, long long jc, double& a0, double& a1, double& c0,
@@ -957,7 +975,7 @@ void launch_win(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, cudaS
 // shared memory per team, fewer teams per SM) or each rank's column is evaluated in place.
 template <int NW, bool PRE>
 __host__ __device__ constexpr size_t smooth_stride() {
-  return (PRE ? static_cast<size_t>(16) * (NW * 64 + 1) : static_cast<size_t>(NW * 64 + 1)) +
+  return (PRE ? static_cast<size_t>(16) * (NW * 64 + 1) : static_cast<size_t>(NW * 64 + 1) + 64) +
          static_cast<size_t>(2) * 16 * NW * 64 + 4 + 4 * NW + 8;
 }
 
@@ -971,9 +989,10 @@ __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntr
   if (team >= teams_per_cta) return;
   double* base = smem + static_cast<size_t>(team) * smooth_stride<NW, PRE>();
   double* s_col = base;                 // PRE: KC x CS raw candidate columns A(i, c); else 1 x CS scratch
-  double* s_v = s_col + (PRE ? KC : 1) * CS;  // KC x NCAP: v_l[j]
+  double* s_v = s_col + (PRE ? KC * CS : CS + 64);  // KC x NCAP: v_l[j]
   double* s_u = s_v + KC * NCAP;        // KC x NCAP: u_l[i] (no dynamic register indexing)
   double* s_yp = s_u + KC * NCAP;       // the pivot row's point
+  double* s_cc = s_col + CS;            // (!PRE) points of the k candidate columns, KC x 4
   double* s_red = s_yp + 4;             // NW x 4: per-warp sum, nz, bv, bi
   double* s_misc = s_red + 4 * NW;      // [0] job [1] pivot value [2] exact verdict [3] scale
   const double kEps0sq = 1e-14 * 1e-14;
@@ -993,6 +1012,19 @@ __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntr
     for (int a = 0; a < DIM; ++a) {
       y0[a] = rv0 ? __ldg(E.coords + a * E.n + rl + t) : 0.0;
       y1[a] = rv1 ? __ldg(E.coords + a * E.n + rl + t + TT) : 0.0;
+    }
+    // the points of this thread's two columns (row pass) stay in registers; the k candidate
+    // columns' points go to shared memory: no global loads on the per-rank critical path
+    double yc0[DIM], yc1[DIM];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      yc0[a] = t < n ? __ldg(E.coords + a * E.n + cl + t) : 0.0;
+      yc1[a] = t + TT < n ? __ldg(E.coords + a * E.n + cl + t + TT) : 0.0;
+    }
+    if constexpr (!PRE) {
+      if (t < KC && t < n)
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) s_cc[t * 4 + a] = yc0[a];
     }
     // raw candidate columns 0 .. min(k, n) - 1, two columns (four entries) at a time
     const int ncol = min(kmax, n);
@@ -1021,7 +1053,10 @@ __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntr
         a0 = s_col[r * CS + t];
         a1 = rv1 ? s_col[r * CS + t + TT] : 0.0;
       } else {
-        E.eval2(y0, y1, cl + r, a0, a1);
+        double pc[DIM];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) pc[a] = s_cc[r * 4 + a];
+        E.phi2(E.r2_pts(y0, pc), E.r2_pts(y1, pc), a0, a1);
         if (!rv1) a1 = 0.0;
       }
       SmoothChain<KC>::col2s<NCAP>(a0, a1, s_u + t, s_u + t + TT, r, s_v + r);
@@ -1150,7 +1185,7 @@ __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntr
         const int j0 = t, j1 = t + TT;
         const bool cv0 = j0 < n, cv1 = j1 < n;
         double b0, b1;
-        E.eval2c(yp, cl + (cv0 ? j0 : 0), cl + (cv1 ? j1 : 0), b0, b1);
+        E.phi2(E.r2_pts(yp, yc0), E.r2_pts(yp, yc1), b0, b1);
         SmoothChain<KC>::row2<NCAP, NCAP>(b0, b1, s_u + p, s_v + j0, s_v + j1, r);
         if (cv0) s_v[r * NCAP + j0] = b0;
         if (cv1) s_v[r * NCAP + j1] = b1;
@@ -2012,7 +2047,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
   double* s_part = s_vc + KC * KC;        // 2 x 4: CTA partial (rank parity)
   double* s_red = s_part + 8;             // 8 warps x 4
   double* s_up = s_red + 32;              // KC: u_l[p]
-  double* s_misc = s_up + KC;             // [0] job
+  double* s_misc = s_up + KC;             // [0] job [1] pivot value
+  double* s_cc = s_misc + 8;              // KC x 4: points of the candidate columns
   const int t = threadIdx.x, lane = t & 31, wib = t >> 5;
   const double kEps0sq = 1e-14 * 1e-14;
   const int kmax = J.kmax;
@@ -2036,6 +2072,18 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
       y1[a] = rv1 ? __ldg(E.coords + a * E.n + rl + i1) : 0.0;
     }
     double* V = J.V + (J.v_off[b] - J.v_base);
+    // the points of this thread's row-pass columns in registers, the candidate columns' in
+    // shared memory: no global loads on the per-rank critical path but the pivot's point
+    double yc0[DIM], yc1[DIM];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      yc0[a] = row0 + t < n ? __ldg(E.coords + a * E.n + cl + row0 + t) : 0.0;
+      yc1[a] = row0 + t + TT < n ? __ldg(E.coords + a * E.n + cl + row0 + t + TT) : 0.0;
+    }
+    if (t < KC && t < n)
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) s_cc[t * 4 + a] = __ldg(E.coords + a * E.n + cl + t);
+    __syncthreads();
     bool used0 = false, used1 = false;
     double s_lo = 0.0, s_hi = 0.0;
     const double gm = static_cast<double>(m) * 1.2e-16;
@@ -2046,7 +2094,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
       const int par = r & 1;
       // column r residual of the own rows (candidate column r: no rejection so far)
       double a0, a1;
-      E.eval2(y0, y1, cl + r, a0, a1);
+      {
+        double pc[DIM];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) pc[a] = s_cc[r * 4 + a];
+        E.phi2(E.r2_pts(y0, pc), E.r2_pts(y1, pc), a0, a1);
+      }
       SmoothChain<KC>::col2s<NCAP, KC>(a0, a1, s_u + t, s_u + t + TT, r, s_vc + r);
       // publish the residuals (the pivot value is read from its owner after the barrier)
       s_res[par * NCAP + t] = a0;
@@ -2156,14 +2209,16 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
         const bool cv0 = j0 < n, cv1 = j1 < n;
         const int jj0 = cv0 ? j0 : 0, jj1 = cv1 ? j1 : 0;
         double b0, b1;
-        E.eval2c(yp, cl + jj0, cl + jj1, b0, b1);
+        E.phi2(E.r2_pts(yp, yc0), E.r2_pts(yp, yc1), b0, b1);
         SmoothChain<KC>::row2<1>(b0, b1, s_up, V + static_cast<long long>(jj0) * kmax,
                                  V + static_cast<long long>(jj1) * kmax, r);
         if (cv0) V[static_cast<long long>(j0) * kmax + r] = b0;
         if (cv1) V[static_cast<long long>(j1) * kmax + r] = b1;
         if (t < KC && t < n) {  // v_r at candidate column t (this CTA's copy)
-          double c0, c1;
-          E.eval2c(yp, cl + t, cl + t, c0, c1);
+          double c0, c1, pc[DIM];
+#pragma unroll
+          for (int a = 0; a < DIM; ++a) pc[a] = s_cc[t * 4 + a];
+          E.phi2(E.r2_pts(yp, pc), E.r2_pts(yp, pc), c0, c1);
           SmoothChain<KC>::row2<KC>(c0, c1, s_up, s_vc + t, s_vc + t, r);
           s_vc[r * KC + t] = c0;
         }
@@ -2215,7 +2270,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
 template <int DIM, int KIND, int CL>
 void launch_smooth_cluster(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, cudaStream_t s) {
   if (J.njobs <= 0) return;
-  const size_t smem = sizeof(double) * (16 * 512 + 2 * 512 + 16 * 16 + 8 + 32 + 16 + 8);
+  const size_t smem = sizeof(double) * (16 * 512 + 2 * 512 + 16 * 16 + 8 + 32 + 16 + 8 + 64);
   auto kfn = aca_smooth_cluster_kernel<DIM, KIND, CL>;
   HM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const long long clusters = std::min<long long>(J.njobs, std::max(1, 2 * sms / CL));

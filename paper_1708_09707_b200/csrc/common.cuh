@@ -148,6 +148,15 @@ void parallel_blocks(long long n, F&& f, int threads = 16) {
   for (auto& th : pool) th.join();
 }
 
+// f(task) for task in [0, n), one host thread per task (coarse tasks, n small)
+template <class F>
+void parallel_tasks(int n, F&& f) {
+  std::vector<std::thread> pool;
+  for (int q = 1; q < n; ++q) pool.emplace_back([&f, q] { f(q); });
+  if (n > 0) f(0);
+  for (auto& th : pool) th.join();
+}
+
 inline unsigned grid_for(long long n, int threads, long long cap = 1ll << 30) {
   long long g = (n + threads - 1) / threads;
   if (g < 1) g = 1;

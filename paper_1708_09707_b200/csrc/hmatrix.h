@@ -199,6 +199,9 @@ void gather_multi(HMatrix& h, const double* X, long long ldx, int R, cudaStream_
 void scatter_multi(HMatrix& h, double* Z, long long ldz, int R, cudaStream_t s);
 void mvp_multi_morton(HMatrix& h, int R, int flags, cudaStream_t s);
 
+// large host -> device copy through the pinned staging ring (setup.cu); synchronous
+void upload_staged(void* dst, const void* src, size_t bytes, cudaStream_t s);
+
 // components
 void morton_codes_device(const double* coords, long long n, int d, unsigned long long* codes, cudaStream_t s);
 // schedule of aca leaves [c0, c1) into h.sched_* at c.sched_off (setup time, may sync)

@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(128) rows_multi_kernel(MArgs a) {
 // per-row kernel to 8 warps per SM).  Per leaf the thread's u_l are issued 4 ranks ahead;
 // the folds are the reference's: y_r = ((0 + u_0 t_0r) + u_1 t_1r) + ..., z_r += y_r in
 // leaf order (aca.cpp:616, hmatrix.cpp:96-113) -- bitwise the one-thread version.
-__global__ void __launch_bounds__(128, 6) rows_multi_far16_kernel(MArgs a) {
+__global__ void __launch_bounds__(128, 4) rows_multi_far16_kernel(MArgs a) {
   constexpr int RH = 8;
   const long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   const long long i = a.row_begin + (g >> 1);
@@ -299,17 +299,24 @@ __global__ void __launch_bounds__(128, 6) rows_multi_far16_kernel(MArgs a) {
 #pragma unroll
       for (int r = 0; r < RH; ++r) y[r] = 0.0;
       for (int l0 = 0; l0 < ke; l0 += 4) {
+        // the group's u and t loads all issued before the first fold step (one latency per
+        // group instead of one per rank)
         double uv[4];
+        double2 tv[4][RH / 2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) uv[q] = l0 + q < ke ? __ldcs(u + uidx(l0 + q)) : 0.0;
+        for (int q = 0; q < 4; ++q) {
+          uv[q] = l0 + q < ke ? __ldcs(u + uidx(l0 + q)) : 0.0;
+#pragma unroll
+          for (int r2 = 0; r2 < RH / 2; ++r2)
+            tv[q][r2] = l0 + q < ke ? __ldg(t2 + (l0 + q) * 8 + r2) : make_double2(0.0, 0.0);
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           if (l0 + q < ke) {
 #pragma unroll
             for (int r2 = 0; r2 < RH / 2; ++r2) {
-              const double2 tv = __ldg(t2 + (l0 + q) * 8 + r2);
-              y[2 * r2] = hadd(y[2 * r2], hmul(uv[q], tv.x));
-              y[2 * r2 + 1] = hadd(y[2 * r2 + 1], hmul(uv[q], tv.y));
+              y[2 * r2] = hadd(y[2 * r2], hmul(uv[q], tv[q][r2].x));
+              y[2 * r2 + 1] = hadd(y[2 * r2 + 1], hmul(uv[q], tv[q][r2].y));
             }
           }
         }

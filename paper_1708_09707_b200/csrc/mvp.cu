@@ -1419,6 +1419,16 @@ void rank_sums(HMatrix& h, const int* ke, long long lo, long long hi) {
 // admissible leaves; in precompute mode also the factors themselves.
 void plan_far_field(HMatrix& h, cudaStream_t s) {
   const long long kmax = h.cfg.k;
+  const bool ptrace = std::getenv("HM_TRACE") != nullptr;
+  auto pt0 = std::chrono::steady_clock::now();
+  auto pmark = [&](const char* what) {
+    if (!ptrace) return;
+    HM_CUDA(cudaStreamSynchronize(s));
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[hm_trace] plan %-28s %8.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - pt0).count());
+    pt0 = now;
+  };
   auto& uo = h.h_uoff;
   auto& vo = h.h_voff;
   uo.resize(h.aca.count + 1);
@@ -1430,39 +1440,37 @@ void plan_far_field(HMatrix& h, cudaStream_t s) {
     const int nb = 16;
     std::vector<long long> bu(nb + 1, 0), bv(nb + 1, 0);
     const long long per = (cnt + nb - 1) / nb;
-    parallel_blocks(nb, [&](long long b0, long long b1) {
-      for (long long q = b0; q < b1; ++q) {
-        long long su = 0, sv = 0;
-        for (long long b = q * per; b < std::min(cnt, (q + 1) * per); ++b) {
-          su += h.aca.h_m[b];
-          sv += h.aca.h_n[b];
-        }
-        bu[q + 1] = su;
-        bv[q + 1] = sv;
+    parallel_tasks(nb, [&](int q) {
+      long long su = 0, sv = 0;
+      for (long long b = q * per; b < std::min(cnt, (q + 1) * per); ++b) {
+        su += h.aca.h_m[b];
+        sv += h.aca.h_n[b];
       }
-    }, nb);
+      bu[q + 1] = su;
+      bv[q + 1] = sv;
+    });
     for (int q = 0; q < nb; ++q) {
       bu[q + 1] += bu[q];
       bv[q + 1] += bv[q];
     }
-    parallel_blocks(nb, [&](long long b0, long long b1) {
-      for (long long q = b0; q < b1; ++q) {
-        long long su = bu[q] * kmax, sv = bv[q] * kmax;
-        for (long long b = q * per; b < std::min(cnt, (q + 1) * per); ++b) {
-          uo[b] = su;
-          vo[b] = sv;
-          su += kmax * h.aca.h_m[b];
-          sv += kmax * h.aca.h_n[b];
-        }
+    parallel_tasks(nb, [&](int q) {
+      long long su = bu[q] * kmax, sv = bv[q] * kmax;
+      for (long long b = q * per; b < std::min(cnt, (q + 1) * per); ++b) {
+        uo[b] = su;
+        vo[b] = sv;
+        su += kmax * h.aca.h_m[b];
+        sv += kmax * h.aca.h_n[b];
       }
-    }, nb);
+    });
     uo[cnt] = bu[nb] * kmax;
     vo[cnt] = bv[nb] * kmax;
   }
   h.u_off.alloc(uo.size(), s);
   h.v_off.alloc(vo.size(), s);
-  HM_CUDA(cudaMemcpyAsync(h.u_off.get(), uo.data(), sizeof(long long) * uo.size(), cudaMemcpyHostToDevice, s));
-  HM_CUDA(cudaMemcpyAsync(h.v_off.get(), vo.data(), sizeof(long long) * vo.size(), cudaMemcpyHostToDevice, s));
+  pmark("offset prefix sums");
+  upload_staged(h.u_off.get(), uo.data(), sizeof(long long) * uo.size(), s);
+  upload_staged(h.v_off.get(), vo.data(), sizeof(long long) * vo.size(), s);
+  pmark("offset upload");
   h.k_eff.alloc(std::max(h.aca.count, 1ll), s);
   h.k_eff.zero(s);
   h.row_piv.alloc(std::max(h.aca.count * kmax, 1ll), s);
@@ -1505,55 +1513,82 @@ void plan_far_field(HMatrix& h, cudaStream_t s) {
   h.chunks.clear();
   h.n_batches = 0;
   {
+    // O(batches log) with binary searches on the offset prefix sums (uo = k * prefix of m,
+    // 8 (uo + vo) = prefix of the factor bytes) instead of a pass over every leaf
+    auto bytes_at = [&](long long j) { return 8 * (uo[j] + vo[j]); };
+    auto rows_at = [&](long long j) { return uo[j] / kmax; };
+    // last j in (b, hi] with f(j) - f(b) <= cap, at least b + 1
+    auto reach = [&](long long b, long long cap, auto f) {
+      long long a = b + 1, z = hi;  // answer in [a, z]
+      const long long base = f(b);
+      if (f(a) - base > cap) return a;
+      while (a < z) {
+        const long long mid = a + (z - a + 1) / 2;
+        if (f(mid) - base <= cap) a = mid;
+        else z = mid - 1;
+      }
+      return a;
+    };
     AcaChunk cur;
     cur.c0 = cur.c1 = lo;
-    long long cbytes = 0;
-    long long b = lo;
-    while (b < hi) {
-      // next reference batch [b, e)
-      long long e = b, rows = 0, bytes = 0;
-      while (e < hi) {
-        const long long m = h.aca.h_m[e];
-        if (e > b && (h.cfg.bs_aca <= 0 || rows + m > h.cfg.bs_aca)) break;
-        rows += m;
-        bytes += 8 * kmax * (h.aca.h_m[e] + h.aca.h_n[e]);
-        ++e;
+    if (h.cfg.bs_aca <= 0) {
+      // one block per batch: chunks are maximal runs of blocks within the budget
+      h.n_batches = hi - lo;
+      long long b = lo;
+      while (b < hi) {
+        const long long e = reach(b, budget, bytes_at);
+        AcaChunk c;
+        c.c0 = b;
+        c.c1 = e;
+        h.chunks.push_back(c);
+        b = e;
       }
-      ++h.n_batches;
-      if (cur.c1 > cur.c0 && cbytes + bytes > budget) {
-        h.chunks.push_back(cur);
-        cur = AcaChunk{};
-        cur.c0 = cur.c1 = b;
-        cbytes = 0;
+    } else {
+      long long cbytes = 0, b = lo;
+      while (b < hi) {
+        const long long e = reach(b, h.cfg.bs_aca, rows_at);  // next reference batch [b, e)
+        const long long bytes = bytes_at(e) - bytes_at(b);
+        ++h.n_batches;
+        if (cur.c1 > cur.c0 && cbytes + bytes > budget) {
+          h.chunks.push_back(cur);
+          cur = AcaChunk{};
+          cur.c0 = cur.c1 = b;
+          cbytes = 0;
+        }
+        cur.c1 = e;
+        cbytes += bytes;
+        b = e;
       }
-      cur.c1 = e;
-      cbytes += bytes;
-      b = e;
+      if (cur.c1 > cur.c0) h.chunks.push_back(cur);
     }
-    if (cur.c1 > cur.c0) h.chunks.push_back(cur);
   }
+  pmark("allocs + batches/chunks");
   h.sched_jobs.alloc(std::max(hi - lo, 1ll), s);
   h.sched_order.alloc(std::max(hi - lo, 1ll), s);
-  for (AcaChunk& c : h.chunks) {
-    c.sched_off = c.c0 - lo;
-    c.ub = uo[c.c0];
-    c.vb = vo[c.c0];
-    c.ue = uo[c.c1];
-    c.ve = vo[c.c1];
-    c.row_lo = h.aca.h_rl[c.c0];
-    std::mutex mu;
-    long long row_hi = 0;
-    parallel_blocks(c.c1 - c.c0, [&](long long b0, long long b1) {
-      long long mx = 0;
-      for (long long b = c.c0 + b0; b < c.c0 + b1; ++b)
-        mx = std::max<long long>(mx, static_cast<long long>(h.aca.h_rl[b]) + h.aca.h_m[b]);
-      std::lock_guard<std::mutex> lk(mu);
-      row_hi = std::max(row_hi, mx);
+  {
+    // chunk row ranges, chunks spread over the host threads (one scan of the leaves)
+    const int nch = static_cast<int>(h.chunks.size());
+    const int nt = std::max(1, std::min(16, nch));
+    parallel_tasks(nt, [&](int q) {
+      for (int ci = q; ci < nch; ci += nt) {
+        AcaChunk& c = h.chunks[ci];
+        c.sched_off = c.c0 - lo;
+        c.ub = uo[c.c0];
+        c.vb = vo[c.c0];
+        c.ue = uo[c.c1];
+        c.ve = vo[c.c1];
+        c.row_lo = h.aca.h_rl[c.c0];
+        long long mx = 0;
+        for (long long b = c.c0; b < c.c1; ++b)
+          mx = std::max<long long>(mx, static_cast<long long>(h.aca.h_rl[b]) + h.aca.h_m[b]);
+        c.row_hi = mx;
+      }
     });
-    c.row_hi = row_hi;
   }
+  pmark("chunk row ranges");
   if (!plan_aca_chunks_all(h, lo, hi, s))
     for (AcaChunk& c : h.chunks) plan_aca_chunk(h, c, s);
+  pmark("schedules (global sorts)");
   if (h.cfg.precompute_aca) {
     const auto t0 = std::chrono::steady_clock::now();
     h.U.alloc(std::max(uo[hi] - uo[lo], 1ll), s);

@@ -394,10 +394,64 @@ void build_spans(HMatrix& h, cudaStream_t s) {
   }
 }
 
-// Device array -> host mirror through a process-wide page-locked staging ring: each 32 MB
-// piece is DMA'd at full link rate and copied out by the host threads (which also take the
-// first-touch page faults of the fresh mirror in parallel), while the next piece is in
-// flight.  Small arrays copy directly.
+// Host <-> device copies of large arrays through a process-wide page-locked staging ring:
+// each 32 MB piece is DMA'd at full link rate while the host threads copy the neighbouring
+// piece (and take the first-touch page faults of a fresh host array in parallel).  Small
+// copies go direct.
+namespace {
+struct StagingRing {
+  static constexpr size_t kPiece = size_t(32) << 20;
+  std::mutex mu;
+  char* ring[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  void ready() {
+    for (int q = 0; q < 2; ++q) {
+      if (!ring[q]) HM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ring[q]), kPiece));
+      if (!done[q]) HM_CUDA(cudaEventCreateWithFlags(&done[q], cudaEventDisableTiming));
+    }
+  }
+  static void host_copy(char* to, const char* from, size_t len) {
+    parallel_blocks(static_cast<long long>(len), [&](long long b0, long long b1) {
+      std::memcpy(to + b0, from + b0, static_cast<size_t>(b1 - b0));
+    }, 8);
+  }
+  void to_host(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(mu);
+    ready();
+    const size_t np = (bytes + kPiece - 1) / kPiece;
+    auto issue = [&](size_t p) {
+      const size_t off = p * kPiece, len = std::min(kPiece, bytes - off);
+      HM_CUDA(cudaMemcpyAsync(ring[p & 1], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost, s));
+      HM_CUDA(cudaEventRecord(done[p & 1], s));
+    };
+    issue(0);
+    for (size_t p = 0; p < np; ++p) {
+      if (p + 1 < np) issue(p + 1);
+      HM_CUDA(cudaEventSynchronize(done[p & 1]));
+      const size_t off = p * kPiece, len = std::min(kPiece, bytes - off);
+      host_copy(static_cast<char*>(dst) + off, ring[p & 1], len);
+    }
+  }
+  void to_device(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(mu);
+    ready();
+    const size_t np = (bytes + kPiece - 1) / kPiece;
+    for (size_t p = 0; p < np; ++p) {
+      const size_t off = p * kPiece, len = std::min(kPiece, bytes - off);
+      if (p >= 2) HM_CUDA(cudaEventSynchronize(done[p & 1]));  // this buffer's previous DMA is done
+      host_copy(ring[p & 1], static_cast<const char*>(src) + off, len);
+      HM_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, ring[p & 1], len, cudaMemcpyHostToDevice, s));
+      HM_CUDA(cudaEventRecord(done[p & 1], s));
+    }
+    HM_CUDA(cudaStreamSynchronize(s));
+  }
+};
+StagingRing& staging() {
+  static StagingRing r;
+  return r;
+}
+}  // namespace
+
 void mirror_to_host(int* dst, const int* src, long long cnt, cudaStream_t s) {
   if (cnt <= 0) return;
   const size_t bytes = sizeof(int) * static_cast<size_t>(cnt);
@@ -406,33 +460,9 @@ void mirror_to_host(int* dst, const int* src, long long cnt, cudaStream_t s) {
     HM_CUDA(cudaStreamSynchronize(s));
     return;
   }
-  constexpr size_t kPiece = size_t(32) << 20;
-  static std::mutex mu;
-  static char* ring[2] = {nullptr, nullptr};
-  static cudaEvent_t done[2] = {nullptr, nullptr};
-  std::lock_guard<std::mutex> lk(mu);
-  for (int q = 0; q < 2; ++q) {
-    if (!ring[q]) HM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ring[q]), kPiece));
-    if (!done[q]) HM_CUDA(cudaEventCreateWithFlags(&done[q], cudaEventDisableTiming));
-  }
-  const size_t npieces = (bytes + kPiece - 1) / kPiece;
-  auto issue = [&](size_t p) {
-    const size_t off = p * kPiece, len = std::min(kPiece, bytes - off);
-    HM_CUDA(cudaMemcpyAsync(ring[p & 1], reinterpret_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost, s));
-    HM_CUDA(cudaEventRecord(done[p & 1], s));
-  };
-  issue(0);
-  for (size_t p = 0; p < npieces; ++p) {
-    if (p + 1 < npieces) issue(p + 1);
-    HM_CUDA(cudaEventSynchronize(done[p & 1]));
-    const size_t off = p * kPiece, len = std::min(kPiece, bytes - off);
-    const char* from = ring[p & 1];
-    char* to = reinterpret_cast<char*>(dst) + off;
-    parallel_blocks(static_cast<long long>(len), [&](long long b0, long long b1) {
-      std::memcpy(to + b0, from + b0, static_cast<size_t>(b1 - b0));
-    }, 8);
-  }
+  staging().to_host(dst, src, bytes, s);
 }
+
 
 void alloc_list(LeafList& l, long long cnt, long long nslots, cudaStream_t s) {
   l.count = cnt;
@@ -459,6 +489,15 @@ void grow(DevBuf<T>& b, size_t need, size_t keep, cudaStream_t s) {
 }
 
 }  // namespace
+
+void upload_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes < (size_t(8) << 20)) {
+    HM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    HM_CUDA(cudaStreamSynchronize(s));  // pageable source: completes before return anyway
+    return;
+  }
+  staging().to_device(dst, src, bytes, s);
+}
 
 void morton_codes_device(const double* coords, long long n, int d, unsigned long long* codes, cudaStream_t s) {
   morton_kernel<<<grid_for(n, 256, 1 << 16), 256, 0, s>>>(coords, n, d, codes);
