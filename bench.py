@@ -11,7 +11,8 @@ larger than the 126 MB L2, so no flush is needed between steps.
   value     = 2 (S_d + S_l) / t  [GFLOP/s, algorithmic, SURVEY.md §8d], whole job
   e2e       = same metric through hm_mvp (C ABI) with host x/z, H2D + D2H inside
   roofline  = dominant kernel (the row-gather product kernel) vs measured HBM peak
-  build_s   = hm_setup wall time (Morton + tree + ACA factors + dense blocks)
+  build_s   = hm_setup wall time (Morton + tree + ACA factors + dense blocks), median of
+              --build-reps constructions
 
 N > 1: rows are partitioned by depth-log2(N) row clusters, every rank
 computes its slice, NCCL allgathers y; N is fixed -> strong scaling.  Launched under
@@ -55,6 +56,8 @@ def parse():
     ap.add_argument("--cpu-baseline", dest="cpu_baseline", type=int, default=1,
                     help="time the reference on the host cores beside the GPU number (rank 0, N=1)")
     ap.add_argument("--cpu-workers", dest="cpu_workers", type=int, default=0)
+    ap.add_argument("--build-reps", dest="build_reps", type=int, default=3,
+                    help="constructions timed; build_s is their median")
     return ap.parse_args()
 
 
@@ -339,9 +342,17 @@ def run_ours(args):
                                                                    precompute_aca=stored, near_stored=stored,
                                                                    device=local)).close()
     warmup_setup_s = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    h = hm.setup(pts, kern, cfg)
-    build_s = time.perf_counter() - t0
+    # the construction is timed build_reps times (each handle closed before the next) and the
+    # median reported: large device allocations / frees make single builds jitter by 0.1-1 s
+    builds = []
+    h = None
+    for _ in range(max(1, args.build_reps)):
+        if h is not None:
+            h.close()
+        t0 = time.perf_counter()
+        h = hm.setup(pts, kern, cfg)
+        builds.append(time.perf_counter() - t0)
+    build_s = sorted(builds)[len(builds) // 2]
     if world > 1:
         uid = hm.nccl_unique_id() if rank == 0 else bytes(128)
         obj = [uid]
@@ -519,7 +530,7 @@ def run_ours(args):
                        "parallelism": f"row-cluster x{world}" if world > 1 else "single",
                        "l2": f"no flush: stored operator {alg_bytes / 1e9:.1f} GB >> 126 MB L2"},
             "hbm_gbs": moved_bytes / (ms_step * 1e-3) / 1e9, "hbm_gbs_reference_layout": hbm, "build_s": build_s,
-            "first_setup_in_process_s": warmup_setup_s,
+            "first_setup_in_process_s": warmup_setup_s, "build_s_all": builds,
             "build_phases_ms": {k: tms[k] for k in ("morton_ms", "tree_ms", "aca_ms", "near_ms", "setup_ms")},
             "work": {"S_d": S_d, "S_d_stored": st["S_d_stored"], "near_sym": sym, "S_l": S_l, "S_lm": S_lm,
                      "S_ln": S_ln, "flops_per_step": flops, "moved_bytes_per_step": moved_bytes,

@@ -229,24 +229,19 @@ __device__ __forceinline__ bool log_main_ok(double x) {
 __device__ __forceinline__ void bessel_k1_series_x2(double x0, double x1, double& k0, double& k1) {
   const double q0 = hmul(hmul(0.25, x0), x0), q1 = hmul(hmul(0.25, x1), x1);
   double t0 = 1.0, t1 = 1.0, si0 = 0.0, si1 = 0.0, sk0 = 0.0, sk1 = 0.0;
-  bool a0 = true, a1 = true;
-  for (int j = 0; j < 64 && (a0 || a1); ++j) {
+  // Branch-free body: a value whose series has stopped gets term 0, so its further steps
+  // add +-0 to sums that are already nonzero (sum_i1 >= 1; sum_k gets -0 only at j = 0,
+  // where the term is 1) and keep the term at 0 -- bitwise the reference's `break`.
+#pragma unroll 1
+  for (int j = 0; j < 64 && (t0 != 0.0 || t1 != 0.0); ++j) {
     const double psi = kK1Dev.psi[j], den = kK1Dev.den[j], rden = kK1Dev.rden[j];
-    const double ni0 = hadd(si0, t0), ni1 = hadd(si1, t1);
-    const double nk0 = hadd(sk0, hmul(psi, t0)), nk1 = hadd(sk1, hmul(psi, t1));
+    si0 = hadd(si0, t0);
+    si1 = hadd(si1, t1);
+    sk0 = hadd(sk0, hmul(psi, t0));
+    sk1 = hadd(sk1, hmul(psi, t1));
     const double nx0 = div_by_const(hmul(t0, q0), den, rden), nx1 = div_by_const(hmul(t1, q1), den, rden);
-    if (a0) {
-      si0 = ni0;
-      sk0 = nk0;
-      if (k1_series_exit(nx0, si0)) a0 = false;
-      else t0 = nx0;
-    }
-    if (a1) {
-      si1 = ni1;
-      sk1 = nk1;
-      if (k1_series_exit(nx1, si1)) a1 = false;
-      else t1 = nx1;
-    }
+    t0 = k1_series_exit(nx0, si0) ? 0.0 : nx0;
+    t1 = k1_series_exit(nx1, si1) ? 0.0 : nx1;
   }
   const double i10 = hmul(hmul(0.5, x0), si0), i11 = hmul(hmul(0.5, x1), si1);
   const double h0 = hmul(0.5, x0), h1 = hmul(0.5, x1);
@@ -261,31 +256,25 @@ __device__ __forceinline__ void bessel_k1_series_x2(double x0, double x1, double
 template <int V>
 __device__ __forceinline__ void bessel_k1_series_xv(const double (&x)[V], double (&kv)[V]) {
   double q[V], t[V], si[V], sk[V];
-  bool act[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     q[v] = hmul(hmul(0.25, x[v]), x[v]);
     t[v] = 1.0;
     si[v] = 0.0;
     sk[v] = 0.0;
-    act[v] = true;
   }
   bool any = true;
-  for (int j = 0; j < 64 && any; ++j) {
+#pragma unroll 1
+  for (int j = 0; j < 64 && any; ++j) {  // branch-free body, as bessel_k1_series_x2
     const double psi = kK1Dev.psi[j], den = kK1Dev.den[j], rden = kK1Dev.rden[j];
     any = false;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      const double ni = hadd(si[v], t[v]);
-      const double nk = hadd(sk[v], hmul(psi, t[v]));
+      si[v] = hadd(si[v], t[v]);
+      sk[v] = hadd(sk[v], hmul(psi, t[v]));
       const double nx = div_by_const(hmul(t[v], q[v]), den, rden);
-      if (act[v]) {
-        si[v] = ni;
-        sk[v] = nk;
-        if (k1_series_exit(nx, ni)) act[v] = false;
-        else t[v] = nx;
-      }
-      any |= act[v];
+      t[v] = k1_series_exit(nx, si[v]) ? 0.0 : nx;
+      any |= t[v] != 0.0;
     }
   }
 #pragma unroll

@@ -1355,6 +1355,16 @@ __global__ void compact_u_kernel(const int* __restrict__ mm, const int* __restri
 static void compact_factors(HMatrix& h, const int* ke, long long lo, long long hi, cudaStream_t s) {
   const long long cnt = hi - lo, kmax = h.cfg.k, S = h.n >> h.dmax_leaf;
   if (cnt <= 0) return;
+  const bool ptrace = std::getenv("HM_TRACE") != nullptr;
+  auto pt0 = std::chrono::steady_clock::now();
+  auto cmark = [&](const char* what) {
+    if (!ptrace) return;
+    HM_CUDA(cudaStreamSynchronize(s));
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[hm_trace] compact %-22s %8.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - pt0).count());
+    pt0 = now;
+  };
   std::vector<long long> uo(cnt + 1, 0), vo(cnt + 1, 0);
   for (long long q = 0; q < cnt; ++q) {
     const long long ke2 = (ke[q] + 1) & ~1;
@@ -1370,12 +1380,16 @@ static void compact_factors(HMatrix& h, const int* ke, long long lo, long long h
   const long long ub = h.h_uoff[lo], vb = h.h_voff[lo];
   {  // V, then U: one old and one new buffer live at a time
     DevBuf<double> V2;
+    cmark("offsets");
     V2.alloc(std::max(vo[cnt], 1ll), s);
+    cmark("alloc V");
     compact_v_kernel<<<grid, 256, 0, s>>>(h.aca.n.get(), h.k_eff.get(), lo, cnt, h.v_off.get(), vb, dvo.get(),
                                           static_cast<int>(kmax), h.V.get(), V2.get());
     HM_LAUNCH_CHECK();
     HM_CUDA(cudaStreamSynchronize(s));
+    cmark("kernel V");
     h.V = std::move(V2);
+    cmark("free old V");
   }
   {
     DevBuf<double> U2;
@@ -1384,7 +1398,9 @@ static void compact_factors(HMatrix& h, const int* ke, long long lo, long long h
                                           static_cast<int>(kmax), static_cast<int>(S), h.U.get(), U2.get());
     HM_LAUNCH_CHECK();
     HM_CUDA(cudaStreamSynchronize(s));
+    cmark("alloc + kernel U");
     h.U = std::move(U2);
+    cmark("free old U");
   }
   // new offsets (relative to the own range; the chunk bases become 0)
   for (long long q = 0; q <= cnt; ++q) {
@@ -1600,12 +1616,14 @@ void plan_far_field(HMatrix& h, cudaStream_t s) {
     }
     for (const AcaChunk& c : h.chunks) compute_aca(h, c, s);
     h.factors_valid = true;
+    pmark("factorisation");
     // S_l with the achieved ranks
     std::vector<int> ke(hi - lo);
     if (hi > lo) HM_CUDA(cudaMemcpyAsync(ke.data(), h.k_eff.get() + lo, sizeof(int) * (hi - lo), cudaMemcpyDeviceToHost, s));
     HM_CUDA(cudaStreamSynchronize(s));
     h.keff_known = true;
     rank_sums(h, ke.data(), lo, hi);
+    pmark("ranks + rank sums");
     if (h.tma_rows && kmax == 16 && std::getenv("HM_NO_COMPACT") == nullptr) compact_factors(h, ke.data(), lo, hi, s);
   }
 }
