@@ -167,6 +167,22 @@ struct KernelEntry {
       a1 = phi_r2(kp, r2b);
     }
   }
+  // three entries from squared distances (bitwise three scalar evaluations)
+  __device__ __forceinline__ void phi3(double r2a, double r2b, double r2c, double& a0, double& a1,
+                                       double& a2) const {
+    if constexpr (KIND >= 0) {
+      const double r2[3] = {r2a, r2b, r2c};
+      double f[3];
+      phi_xv<KIND, 3>(kp, r2, f);
+      a0 = f[0];
+      a1 = f[1];
+      a2 = f[2];
+    } else {
+      a0 = phi_r2(kp, r2a);
+      a1 = phi_r2(kp, r2b);
+      a2 = phi_r2(kp, r2c);
+    }
+  }
   // four entries: row y against points j0, j1 and rows z0, z1 against point jc
   __device__ __forceinline__ void eval4(const double* y, long long j0, long long j1, const double* z0,
                                         const double* z1, long long jc, double& a0, double& a1, double& c0,
@@ -833,6 +849,10 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
 #pragma unroll
             for (int j = 0; j < KC; ++j)
               if (j >= KC - r) s_up[j - (KC - r)] = uR[q][j];
+            if constexpr (DIM > 0) {  // the pivot row's point, from the owner's registers
+#pragma unroll
+              for (int a = 0; a < DIM; ++a) s_misc[4 + a] = y[q][a];
+            }
           }
         }
       }
@@ -851,7 +871,12 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
       ev_row += n;
       {
         double yp[DIM > 0 ? DIM : 20];
-        E.load(rl + p, yp);
+        if constexpr (DIM > 0) {
+#pragma unroll
+          for (int a = 0; a < DIM; ++a) yp[a] = s_misc[4 + a];
+        } else {
+          E.load(rl + p, yp);
+        }
         double uP[KC];  // u_l[p], right-aligned (aca_chain.cuh)
 #pragma unroll
         for (int j = 0; j < KC; ++j) uP[j] = j >= KC - r ? s_up[j - (KC - r)] : 0.0;
@@ -2192,6 +2217,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
       // u_l[p] (l < r) and the pivot value from the owner CTA
       if (t < r) s_up[t] = *rem(s_u + t * NCAP + pl, po);
       if (t == KC) s_misc[1] = *rem(s_res + par * NCAP + pl, po);
+      if (t >= 32 && t < 32 + DIM) s_misc[2 + t - 32] = __ldg(E.coords + (t - 32) * E.n + rl + p);  // pivot point
       if (po == cr && t == (pl % TT)) {
         if (pl >= TT) used1 = true;
         else used0 = true;
@@ -2204,23 +2230,37 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
       {
         double yp[DIM];
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) yp[a] = __ldg(E.coords + a * E.n + rl + p);
+        for (int a = 0; a < DIM; ++a) yp[a] = s_misc[2 + a];
         const int j0 = row0 + t, j1 = row0 + t + TT;
         const bool cv0 = j0 < n, cv1 = j1 < n;
         const int jj0 = cv0 ? j0 : 0, jj1 = cv1 ? j1 : 0;
-        double b0, b1;
-        E.phi2(E.r2_pts(yp, yc0), E.r2_pts(yp, yc1), b0, b1);
+        // v_r at the candidate columns c < k (this CTA's copy): CTA 0 owns those columns
+        // (its lane t < k computes column t below); elsewhere warp 0 evaluates them
+        // interleaved with its own two columns (one 3-way evaluation, not two 2-way ones
+        // in sequence, so warp 0 does not hold the end-of-rank barrier)
+        const bool cand = cr != 0 && wib == 0;
+        double b0, b1, c0 = 0.0;
+        if (cand) {
+          double pc[DIM];
+          const int tc = (t < KC && t < n) ? t : 0;
+#pragma unroll
+          for (int a = 0; a < DIM; ++a) pc[a] = s_cc[tc * 4 + a];
+          E.phi3(E.r2_pts(yp, yc0), E.r2_pts(yp, yc1), E.r2_pts(yp, pc), b0, b1, c0);
+        } else {
+          E.phi2(E.r2_pts(yp, yc0), E.r2_pts(yp, yc1), b0, b1);
+        }
         SmoothChain<KC>::row2<1>(b0, b1, s_up, V + static_cast<long long>(jj0) * kmax,
                                  V + static_cast<long long>(jj1) * kmax, r);
         if (cv0) V[static_cast<long long>(j0) * kmax + r] = b0;
         if (cv1) V[static_cast<long long>(j1) * kmax + r] = b1;
-        if (t < KC && t < n) {  // v_r at candidate column t (this CTA's copy)
-          double c0, c1, pc[DIM];
-#pragma unroll
-          for (int a = 0; a < DIM; ++a) pc[a] = s_cc[t * 4 + a];
-          E.phi2(E.r2_pts(yp, pc), E.r2_pts(yp, pc), c0, c1);
-          SmoothChain<KC>::row2<KC>(c0, c1, s_up, s_vc + t, s_vc + t, r);
-          s_vc[r * KC + t] = c0;
+        if (t < KC && t < n) {
+          if (cr == 0) {
+            s_vc[r * KC + t] = b0;  // column j0 = t: the same chain over the same v_l values
+          } else {
+            double c1 = c0;
+            SmoothChain<KC>::row2<KC>(c0, c1, s_up, s_vc + t, s_vc + t, r);
+            s_vc[r * KC + t] = c0;
+          }
         }
       }
       if (cr == 0 && t == 0) {
