@@ -246,8 +246,9 @@ struct AcaJob {
 // u_hat[i] / pivot (aca.cpp:466-470), correctly rounded: the pivot's correctly rounded
 // reciprocal y and one Markstein correction, q = a*y, r = fma(-q, p, a) (exact),
 // q' = fma(r, y, q) -- the IEEE quotient for operands in [2^-500, 2^500] (checked bit for
-// bit by tests/cpp/div_const_check.c); zeros (sign) and out-of-range operands take the
-// IEEE division.  One reciprocal per rank instead of m full divisions.
+// bit by tests/cpp/div_const_check.c); a zero numerator gives the signed zero, other
+// out-of-range operands take the IEEE division.  One reciprocal per rank instead of m
+// full divisions.
 static __device__ __noinline__ double ieee_div_slow(double a, double p) { return __ddiv_rn(a, p); }
 
 struct PivotDiv {
@@ -260,10 +261,15 @@ struct PivotDiv {
   }
   __device__ __forceinline__ double operator()(double a) const {
     const double aa = fabs(a);
-    if (fast && aa >= 0x1p-500 && aa <= 0x1p500) {
+    // a == 0 is the common case off the fast range: every earlier pivot row's residual is
+    // exactly +0 (its fold repeats v_l's), so each rank would otherwise send a few lanes of
+    // every warp down the out-of-line division.  0 / p is the zero with the xor'ed sign.
+    if (fast && (aa == 0.0 || (aa >= 0x1p-500 && aa <= 0x1p500))) {
       const double q = __dmul_rn(a, y);
       const double r = __fma_rn(-q, p, a);
-      return __fma_rn(r, y, q);
+      const double z = __longlong_as_double((__double_as_longlong(a) ^ __double_as_longlong(p)) &
+                                            static_cast<long long>(0x8000000000000000ull));
+      return aa == 0.0 ? z : __fma_rn(r, y, q);
     }
     return ieee_div_slow(a, p);  // out of line: keeps the hot loops' register footprint
   }
