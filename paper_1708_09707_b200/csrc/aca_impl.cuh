@@ -282,6 +282,20 @@ __device__ __forceinline__ void argmax_combine(double& bv, int& bi, double ov, i
   }
 }
 
+// Warp argmax of non-negative finite values, first (smallest) index on ties, with three
+// redux.sync instructions instead of five shuffle rounds: non-negative doubles order like
+// their bit patterns, so the maximum is (max high word, max low word among those lanes).
+// "No candidate" is (+0, INT_MAX); a zero maximum is rejected by the caller anyway.
+__device__ __forceinline__ void warp_argmax_nonneg(double& bv, int& bi) {
+  const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(bv));
+  const unsigned hi = static_cast<unsigned>(u >> 32), lo = static_cast<unsigned>(u);
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  const bool top = hi == mhi && lo == mlo;
+  bi = static_cast<int>(__reduce_min_sync(0xffffffffu, top ? static_cast<unsigned>(bi) : 0x7fffffffu));
+  bv = __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(mhi) << 32) | mlo));
+}
+
 template <int DIM, bool DENSE>
 __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaJob J, KernelEntry<DIM> E) {
   __shared__ double s_col[kColBuf];
@@ -811,8 +825,9 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
       const int cstar = next - 1;
       const double* acol = s_win + (cstar % W) * PS;
 
-      // pivot row: argmax |u_hat| over unused rows, first index wins (aca.cpp:367, 375-376)
-      double bv = -1.0;
+      // pivot row: argmax |u_hat| over unused rows, first index wins (aca.cpp:367, 375-376);
+      // the column qualified, so the maximum is > 0 and zero rows never matter
+      double bv = 0.0;
       int bi = 0x7fffffff;
 #pragma unroll
       for (int q = 0; q < RPL; ++q) {
@@ -825,12 +840,7 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
           }
         }
       }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        argmax_combine(bv, bi, ov, oi);
-      }
+      warp_argmax_nonneg(bv, bi);
       if constexpr (NW > 1) {
         if (lane == 0) {
           s_rbv[wib] = bv;
@@ -1091,32 +1101,25 @@ __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntr
         if (!rv1) a1 = 0.0;
       }
       SmoothChain<KC>::col2s<NCAP>(a0, a1, s_u + t, s_u + t + TT, r, s_v + r);
-      // fused reduction: norm2 (any order, bounded), nonzero flag, argmax over unused rows
-      double sum = 0.0, bv = -1.0;
-      int nz = 0, bi = 0x7fffffff;
+      // fused reduction: norm2 (any order, bounded), argmax over unused rows; the nonzero
+      // flag is "maximum > 0" (|u_hat| >= 0, no candidate = +0)
+      double sum = 0.0, bv = 0.0;
+      int bi = 0x7fffffff;
       if (rv0) {
         sum = hmul(a0, a0);
         if (!used0) {
-          nz |= fabs(a0) > 0.0 ? 1 : 0;
           bv = fabs(a0);
           bi = t;
         }
       }
       if (rv1) {
         sum = hadd(sum, hmul(a1, a1));
-        if (!used1) {
-          nz |= fabs(a1) > 0.0 ? 1 : 0;
-          argmax_combine(bv, bi, fabs(a1), t + TT);
-        }
+        if (!used1) argmax_combine(bv, bi, fabs(a1), t + TT);
       }
 #pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
-        nz |= __shfl_xor_sync(0xffffffffu, nz, o);
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        argmax_combine(bv, bi, ov, oi);
-      }
+      for (int o = 16; o; o >>= 1) sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+      warp_argmax_nonneg(bv, bi);
+      int nz = bv > 0.0 ? 1 : 0;
       if constexpr (NW > 1) {
         if (lane == 0) {
           s_red[4 * wib] = sum;
@@ -2135,31 +2138,23 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
       // publish the residuals (the pivot value is read from its owner after the barrier)
       s_res[par * NCAP + t] = a0;
       s_res[par * NCAP + t + TT] = a1;
-      double sum = 0.0, bv = -1.0;
-      int nz = 0, bi = 0x7fffffff;
+      double sum = 0.0, bv = 0.0;  // no candidate = +0 (see warp_argmax_nonneg)
+      int bi = 0x7fffffff;
       if (rv0) {
         sum = hmul(a0, a0);
         if (!used0) {
-          nz |= fabs(a0) > 0.0 ? 1 : 0;
           bv = fabs(a0);
           bi = i0;
         }
       }
       if (rv1) {
         sum = hadd(sum, hmul(a1, a1));
-        if (!used1) {
-          nz |= fabs(a1) > 0.0 ? 1 : 0;
-          argmax_combine(bv, bi, fabs(a1), i1);
-        }
+        if (!used1) argmax_combine(bv, bi, fabs(a1), i1);
       }
 #pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
-        nz |= __shfl_xor_sync(0xffffffffu, nz, o);
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        argmax_combine(bv, bi, ov, oi);
-      }
+      for (int o = 16; o; o >>= 1) sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+      warp_argmax_nonneg(bv, bi);
+      int nz = bv > 0.0 ? 1 : 0;
       if (lane == 0) {
         s_red[4 * wib] = sum;
         s_red[4 * wib + 1] = static_cast<double>(nz);
