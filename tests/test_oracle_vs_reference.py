@@ -158,3 +158,29 @@ def test_reference_leaf_sample_driver_equals_reference_mvp(reference, tmp_path):
                          capture_output=True, text=True,
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert out.returncode == 0, out.stderr
+
+
+def test_reference_row_sample_driver_equals_reference_mvp(reference):
+    """The stored-mode reference arm (ref_mvp_rows_timed, oracle/refbench.py) reproduces
+    the reference's own product on the sampled row clusters bitwise (Morton order), with
+    the O(N) permutation hoisted out of the reps and charged pro rata."""
+    import ctypes as C
+    from oracle.refbench import cluster_ranges, leaf_depth
+    n, d, c_leaf = 4096, 2, 32
+    P = uniform_points(n, d, 42)
+    h = reference.setup(P, kernel=0, c_leaf=c_leaf, k=12)
+    _, perm = h.points()
+    x = symmetric(9, n)
+    want = h.mvp(x)[perm]
+    L = reference.lib
+    L.ref_mvp_rows_timed.restype = C.c_int
+    L.ref_mvp_rows_timed.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                                     C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    ranges = np.array(cluster_ranges(n, leaf_depth(n, c_leaf), [0, 5, 77]), dtype=np.int64)
+    z = np.full(n, np.nan)
+    ta, tm, fl = C.c_double(), C.c_double(), C.c_double()
+    assert L.ref_mvp_rows_timed(h.h, x.ctypes.data, ranges.shape[0], ranges.ctypes.data, 2, z.ctypes.data,
+                                C.byref(ta), C.byref(tm), C.byref(fl)) == 0
+    assert tm.value > 0.0 and fl.value > 0.0
+    for lo, hi in ranges:
+        assert np.array_equal(z[lo:hi].view(np.uint64), want[lo:hi].view(np.uint64))
