@@ -245,6 +245,8 @@ void compute_aca(HMatrix& h, const AcaChunk& c, cudaStream_t s) {
     L.smooth_pre = ep ? std::atoi(ep) != 0 : false;
     const char* em = std::getenv("HM_SMOOTH_MID");
     L.smooth_mid = em ? std::atoi(em) != 0 : false;
+    const char* eb = std::getenv("HM_BIG_ONE");
+    L.big_one = eb ? std::atoi(eb) != 0 : h.d >= 3;
   }
   L.fb_list = h.aca_fallback.get();
   L.fb_count = h.aca_counters.get() + kAcaClasses;

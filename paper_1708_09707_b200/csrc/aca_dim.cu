@@ -57,8 +57,9 @@ static void classes_kind(const AcaClassLaunch& L, cudaStream_t s0) {
   }
   tr.mark("clusters (<=4096)", s);
   if (L.J[kAcaBig].njobs > 0) {
-    if (kmax <= 16) launch_big<DIM, KIND, 16>(L.J[kAcaBig], E, L.max_rows_big, sms, *L.big_scratch, s);
-    else launch_big<DIM, KIND, 32>(L.J[kAcaBig], E, L.max_rows_big, sms, *L.big_scratch, s);
+    const bool big_one = L.big_one;
+    if (kmax <= 16) launch_big<DIM, KIND, 16>(L.J[kAcaBig], E, L.max_rows_big, sms, *L.big_scratch, s, big_one);
+    else launch_big<DIM, KIND, 32>(L.J[kAcaBig], E, L.max_rows_big, sms, *L.big_scratch, s, big_one);
     tr.mark("big (>4096)", s);
   }
   s = s0;

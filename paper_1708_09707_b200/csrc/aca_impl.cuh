@@ -1296,7 +1296,7 @@ constexpr int kBigW = 8;
 
 template <int DIM, int KIND, int KC>
 __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, KernelEntry<DIM, KIND> E, double* gscratch,
-                                                              long long gstride, int mask_words) {
+                                                              long long gstride, int mask_words, int smooth1) {
   constexpr int TT = kBigThreads;
   constexpr int W = kBigW;
   constexpr int G = TT / W;  // 32: one warp per column in the qualification pass
@@ -1370,16 +1370,32 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
       scale_exact = true;
     };
 
+    // smooth1 (d >= 3): while the block has rejected nothing, the window is ONE column in
+    // slot 0 (evaluated when it is needed, no cross updates): the per-CTA scratch actually
+    // touched is m doubles, so all resident CTAs' windows stay in L2; the first rejection
+    // switches to the W-column speculative window (filled == 0 at that point).
+    bool one = false, fused_ok = false;
+    int fused_p = 0;
+    double* s_fsum = s_wsum + W;  // 8 warps: fused pass partial norms
+    auto wslot = [&](int col) -> double* { return win + (one ? 0ll : static_cast<long long>(col % W)) * PS; };
     for (int r = 0; r < kmax; ++r) {
       int acc_w = -1;
       double acc_sum = 0.0;
       r_cur = r;
       while (next < n) {
+        one = smooth1 && rejections == 0;
         // speculation depth: while no column was rejected, at most kmax - r more can be
         // accepted (smooth blocks, d >= 3: no noise floor), so do not evaluate past them
-        const int lim = rejections ? W : max(kmax - r, 1);
+        const int lim = rejections ? W : (one ? 1 : max(kmax - r, 1));
         const int wcols = max(filled, min(min(W, lim), n - next));
         ev_col += static_cast<unsigned long long>(wcols - filled) * m;
+        // one-column path: the fill also forms the column's norm2 (any order: bounded), the
+        // nonzero flag and the argmax over unused rows (rows visited in increasing order,
+        // strict >: first index on ties) -- no second and third pass over the column
+        const bool fuse = one && filled == 0 && wcols == 1;
+        double fsum = 0.0, fbv = 0.0;
+        int fbi = 0x7fffffff;
+        fused_ok = false;
         // fill: per row pair, u of the two rows into registers once, then every fresh column
         for (int i0 = t; i0 < m; i0 += 2 * TT) {
           const int i1 = i0 + TT;
@@ -1404,20 +1420,58 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
             if (!ok1) a1 = 0.0;
             if constexpr (kLeft) SmoothChain<16>::col2<1>(a0, a1, uR[0], uR[1], r, V + static_cast<long long>(col) * kmax);
             else Chain<KC>::run2(a0, a1, uR[0], uR[1], r, V + static_cast<long long>(col) * kmax + (r - KC), 1);
-            double* dst = win + static_cast<long long>(col % W) * PS;
+            double* dst = wslot(col);
             dst[i0] = a0;
             if (ok1) dst[i1] = a1;
+            if (fuse) {
+              fsum = hadd(fsum, hmul(a0, a0));
+              if (!is_used(i0) && fabs(a0) > fbv) {
+                fbv = fabs(a0);
+                fbi = i0;
+              }
+              if (ok1) {
+                fsum = hadd(fsum, hmul(a1, a1));
+                if (!is_used(i1) && fabs(a1) > fbv) {
+                  fbv = fabs(a1);
+                  fbi = i1;
+                }
+              }
+            }
           }
         }
         filled = wcols;
+        if (fuse) {
+#pragma unroll
+          for (int o = 16; o; o >>= 1) fsum = hadd(fsum, __shfl_xor_sync(0xffffffffu, fsum, o));
+          warp_argmax_nonneg(fbv, fbi);
+          if (lane == 0) {
+            s_fsum[wib] = fsum;
+            s_rbv[wib] = fbv;
+            s_rbi[wib] = fbi;
+          }
+        }
         __syncthreads();
+        if (fuse) {
+          double sum = s_fsum[0], bv = s_rbv[0];
+          int bi = s_rbi[0];
+          for (int g = 1; g < TT / 32; ++g) {
+            sum = hadd(sum, s_fsum[g]);
+            argmax_combine(bv, bi, s_rbv[g], s_rbi[g]);
+          }
+          if (decide(sum, bv > 0.0 ? 1 : 0) == 1) {
+            acc_w = 0;
+            acc_sum = sum;
+            fused_ok = true;
+            fused_p = bi;
+          }
+        }
         // qualification.  Fast path while the block has rejected nothing: the first window
         // column with the whole CTA (4 loads in flight per thread); otherwise one warp per
         // window column.  Decisions use the rigorous bound of the parallel sums; scale2 is a
         // bracket until an ambiguous decision needs it exactly (resolve_exact).
         int first_state = -1;
-        if (rejections == 0) {
-          const double* src = win + static_cast<long long>(next % W) * PS;
+        if (rejections == 0 && !fuse) {
+          const double* src = wslot(next);
           double sum = 0.0;
           int nz = 0;
           for (int i = t; i < m; i += 4 * TT) {
@@ -1460,7 +1514,7 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
             double sum = 0.0;
             int nz = 0;
             if (w < wcols) {
-              const double* src = win + static_cast<long long>((next + w) % W) * PS;
+              const double* src = wslot(next + w);
               for (int i = lane; i < m; i += 4 * 32) {
                 double a[4];
 #pragma unroll
@@ -1489,7 +1543,7 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
             if (st == 2) {
               resolve_exact();
               if (t == 0) {  // the reference's sequential left fold (aca.cpp:373-374 / 414-415)
-                const double* src = win + static_cast<long long>((next + w) % W) * PS;
+                const double* src = wslot(next + w);
                 double f = hmul(src[0], src[0]);
                 for (int i = 1; i < m; ++i) f = hadd(f, hmul(src[i], src[i]));
                 s_misc[2] = f > hmul(kEps0sq, scale) ? 1.0 : 0.0;
@@ -1520,10 +1574,10 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
       }
       if (acc_w < 0) break;
       const int cstar = next - 1;
-      const double* acol = win + static_cast<long long>(cstar % W) * PS;
+      const double* acol = wslot(cstar);
       double bv = -1.0;
       int bi = 0x7fffffff;
-      for (int i = t; i < m; i += 4 * TT) {
+      for (int i = t; !fused_ok && i < m; i += 4 * TT) {
         double a[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) a[u] = i + u * TT < m ? acol[i + u * TT] : 0.0;
@@ -1545,17 +1599,18 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         argmax_combine(bv, bi, ov, oi);
       }
-      if (lane == 0) {
-        s_rbv[wib] = bv;
-        s_rbi[wib] = bi;
+      if (!fused_ok) {
+        if (lane == 0) {
+          s_rbv[wib] = bv;
+          s_rbi[wib] = bi;
+        }
+        __syncthreads();
+        bv = s_rbv[0];
+        bi = s_rbi[0];
+        for (int g = 1; g < TT / 32; ++g) argmax_combine(bv, bi, s_rbv[g], s_rbi[g]);
       }
-      __syncthreads();
-      bv = s_rbv[0];
-      bi = s_rbi[0];
-      for (int g = 1; g < TT / 32; ++g) argmax_combine(bv, bi, s_rbv[g], s_rbi[g]);
-      const int p = bi;
-      if (t == 0)
-        for (int l = 0; l < r; ++l) s_up[l] = U[uix(l, p)];
+      const int p = fused_ok ? fused_p : bi;
+      for (int l = t; l < r; l += TT) s_up[l] = U[uix(l, p)];
       __syncthreads();
       const PivotDiv pdiv(acol[p]);
       ev_row += n;
@@ -1589,16 +1644,27 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
           if (ok1) V[static_cast<long long>(j1) * kmax + r] = a1;
         }
       }
-      __syncthreads();
+      // (the used-row mask changes before the barrier: the next rank's fused fill reads it)
       if (t == 0) s_mask[p >> 5] |= 1u << (p & 31);
+      __syncthreads();
       {
         // u_r = u_hat / pivot (aca.cpp:466-470) fused with the window cross: per row the
         // accepted column's entry and the W window entries are loaded together, u_r goes
         // to U and straight into the window updates (no reload)
+        if (filled == 0) {  // no window left (always so on the one-column path): 4 loads in flight
+          for (int i = t; i < m; i += 4 * TT) {
+            double a[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[u] = i + u * TT < m ? acol[i + u * TT] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (i + u * TT < m) U[uix(r, i + u * TT)] = pdiv(a[u]);
+          }
+        }
         double vr[W];
 #pragma unroll
         for (int co = 0; co < W; ++co) vr[co] = co < filled ? V[static_cast<long long>(next + co) * kmax + r] : 0.0;
-        for (int i = t; i < m; i += TT) {
+        for (int i = t; filled > 0 && i < m; i += TT) {
           const double ah = acol[i];
           double a[W];
 #pragma unroll
@@ -2321,7 +2387,7 @@ void launch_smooth_cluster(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int
 
 template <int DIM, int KIND, int KC>
 void launch_big(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int max_rows, int sms, DevBuf<double>& scratch,
-                cudaStream_t s) {
+                cudaStream_t s, bool smooth1) {
   if (J.njobs <= 0) return;
   const int mask_words = (max_rows + 31) / 32;
   const size_t smem = ((mask_words + 1) / 2 + kKmax + 40) * sizeof(double);
@@ -2335,7 +2401,8 @@ void launch_big(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int max_rows, 
   const long long gstride = max_rows + 1;
   const size_t need = static_cast<size_t>(gstride) * kBigW * ctas;
   if (scratch.size() < need) scratch.alloc(need, s);
-  kfn<<<static_cast<unsigned>(std::max(ctas, 1ll)), kBigThreads, smem, s>>>(J, E, scratch.get(), gstride, mask_words);
+  kfn<<<static_cast<unsigned>(std::max(ctas, 1ll)), kBigThreads, smem, s>>>(J, E, scratch.get(), gstride, mask_words,
+                                                                            smooth1 ? 1 : 0);
   HM_LAUNCH_CHECK();
 }
 
@@ -2373,6 +2440,7 @@ struct AcaClassLaunch {
   bool smooth_pre = false;     // ... with the candidate columns evaluated up front
   bool smooth_mid = false;     // smooth cluster kernel also for <= 512 / <= 1024 (CL = 1, 2;
                                // measured slower than the window kernels there: off)
+  bool big_one = false;        // big-block kernel: one-column window until a rejection (d >= 3)
   int* fb_list = nullptr;      // per class q at offset first[q]: blocks handed back
   int* fb_count = nullptr;     // kAcaClasses counts
   int* fb_counter = nullptr;   // kAcaClasses job counters of the fallback passes

@@ -39,11 +39,13 @@ def built(gpu, oracle):
         key = (n, d, c_leaf, kind, tuple(sorted(kw.items())))
         if key not in cache:
             P = uniform_points(n, d, 42)
-            cfgkw = dict(c_leaf=c_leaf, k=kw.get("k", 16), epsilon=kw.get("epsilon"))
+            cfgkw = dict(c_leaf=c_leaf, k=kw.get("k", 16), epsilon=kw.get("epsilon"), eta=kw.get("eta", 1.5))
+            bsd = max(1 << 22, c_leaf * c_leaf)  # one dense leaf block must fit a dense batch
             h = gpu.setup(P, gpu.KernelFunction("matern" if kind else "gaussian"),
-                          gpu.HmatrixConfig(**cfgkw, precompute_aca=kw.get("pre", False),
+                          gpu.HmatrixConfig(**cfgkw, bs_dense=bsd, precompute_aca=kw.get("pre", False),
                                             near_stored=kw.get("stored", False)))
-            o = oracle.setup(P, kernel=kind, c_leaf=c_leaf, k=cfgkw["k"], epsilon=cfgkw["epsilon"])
+            o = oracle.setup(P, kernel=kind, c_leaf=c_leaf, k=cfgkw["k"], epsilon=cfgkw["epsilon"], eta=cfgkw["eta"],
+                             bs_dense=bsd)
             cache[key] = (P, h, o)
         return cache[key]
 
@@ -182,18 +184,20 @@ def test_halton_and_force_dense(gpu, oracle):
     assert np.array_equal(bits(h.mvp(x)), bits(o.mvp(x)))
 
 
-@pytest.mark.parametrize("n,d,c_leaf,kind,k", [
-    (1 << 16, 2, 64, 0, 16),   # noise-floor rejections in every size class
-    (5000, 3, 40, 0, 24),      # k > 16: the 32-wide register rank window
-    (6000, 2, 100, 1, 12),     # Matern, non-power-of-two clusters up to 750 wide
-    (60000, 1, 64, 0, 16),     # d = 1: blocks of 15000 rows (global window column of the big kernel)
-    (40000, 2, 100, 0, 24),    # ragged 1250..5000-row blocks: 4- and 8-CTA cluster kernels, k > 16
+@pytest.mark.parametrize("n,d,c_leaf,kind,k,eta", [
+    (1 << 16, 2, 64, 0, 16, 1.5),   # noise-floor rejections in every size class
+    (5000, 3, 40, 0, 24, 1.5),      # k > 16: the 32-wide register rank window
+    (6000, 2, 100, 1, 12, 1.5),     # Matern, non-power-of-two clusters up to 750 wide
+    (60000, 1, 64, 0, 16, 1.5),     # d = 1: blocks of 15000 rows (global window column of the big kernel)
+    (40000, 2, 100, 0, 24, 1.5),    # ragged 1250..5000-row blocks: 4- and 8-CTA cluster kernels, k > 16
+    (100000, 3, 7000, 1, 16, 5.0),  # d = 3 Matern: 6250-row blocks, big kernel's one-column window
+    (100000, 3, 7000, 0, 16, 5.0),  # ... Gaussian
 ])
-def test_aca_size_classes_bitwise(built, n, d, c_leaf, kind, k):
+def test_aca_size_classes_bitwise(built, n, d, c_leaf, kind, k, eta):
     """Every ACA size class (window kernels for max(m,n) <= 64/128/256/512/1024, thread-block
     cluster kernels <= 2048/4096, the big-block kernel beyond) reproduces aca_batched's
     pivots, ranks and factors bit for bit."""
-    P, h, o = built(n, d, c_leaf, kind, k=k)
+    P, h, o = built(n, d, c_leaf, kind, k=k, eta=eta)
     r0 = h.stats()["aca_rejections"]
     fh = h.aca_factors()
     rej = h.stats()["aca_rejections"] - r0
