@@ -583,7 +583,7 @@ __device__ __forceinline__ void team_sync(int team) {
 template <int NW, int KC, int W, bool VSM>
 __host__ __device__ constexpr size_t win_stride() {
   return static_cast<size_t>(W) * (NW * 64 + 1) + (VSM ? static_cast<size_t>(KC) * NW * 64 : 0) + KC + 2 * NW + W +
-         NW * 64 / 8 + 8;
+         NW * 64 / 8 + 8 + 2 * NW;
 }
 
 template <int DIM, int KIND, int NW, int KC, int W, bool VSM, int MINB>
@@ -609,6 +609,8 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
   int* s_state = reinterpret_cast<int*>(s_rbv + 2 * NW);
   unsigned char* s_used = reinterpret_cast<unsigned char*>(s_rbv + 2 * NW + W);
   double* s_misc = s_rbv + 2 * NW + W + NCAP / 8;  // [0] job, [1] scale, [2] exact-fold verdict
+  double* s_fbv = s_misc + 8;                       // NW: fused fast-path argmax (value, index)
+  int* s_fbi = reinterpret_cast<int*>(s_fbv + NW);
   const double kEps0sq = 1e-14 * 1e-14;
   const int kmax = J.kmax;
   const bool kpow2 = (kmax & (kmax - 1)) == 0;
@@ -667,6 +669,11 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
 
     for (int r = 0; r < kmax; ++r) {
       int acc_w = -1;
+      // fast path: the first window column's norm2, nonzero flag and argmax over unused
+      // rows in ONE reduction (the argmax is the pivot when the column qualifies)
+      bool fast_ok = false;
+      double fbv = 0.0;
+      int fbi = 0x7fffffff;
       while (next < n) {
         // speculation depth: while no column was rejected, at most kmax - r more can be
         // accepted (smooth blocks, d >= 3: no noise floor), so do not evaluate past them
@@ -705,35 +712,41 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
         if (rejections == 0) {
           const double* src = s_win + (next % W) * PS;
           double sum = 0.0;
-          int nz = 0;
+          fbv = 0.0;
+          fbi = 0x7fffffff;
 #pragma unroll
-          for (int q = 0; q < RPL; ++q) {
+          for (int q = 0; q < RPL; ++q) {  // rows in increasing order, strict >: first index on ties
             const int i = t + q * TT;
             if (i < m) {
               const double a = src[i];
               sum = hadd(sum, hmul(a, a));
-              nz |= (!s_used[i] && fabs(a) > 0.0) ? 1 : 0;
+              if (!s_used[i] && fabs(a) > fbv) {
+                fbv = fabs(a);
+                fbi = i;
+              }
             }
           }
 #pragma unroll
-          for (int o = 16; o; o >>= 1) {
-            sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
-            nz |= __shfl_xor_sync(0xffffffffu, nz, o);
-          }
+          for (int o = 16; o; o >>= 1) sum = hadd(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+          warp_argmax_nonneg(fbv, fbi);
           if constexpr (NW > 1) {
+            // published in s_rbv / s_fbv, read after ONE barrier; the next writer of these
+            // slots is the next rank's fast path, several barriers later
             if (lane == 0) {
               s_rbv[wib] = sum;
-              s_rbi[wib] = nz;
+              s_fbv[wib] = fbv;
+              s_fbi[wib] = fbi;
             }
             team_sync<NW>(team);
             sum = s_rbv[0];
-            nz = s_rbi[0];
+            fbv = s_fbv[0];
+            fbi = s_fbi[0];
             for (int k2 = 1; k2 < NW; ++k2) {
               sum = hadd(sum, s_rbv[k2]);
-              nz |= s_rbi[k2];
+              argmax_combine(fbv, fbi, s_fbv[k2], s_fbi[k2]);
             }
-            team_sync<NW>(team);
           }
+          const int nz = fbv > 0.0 ? 1 : 0;
           first_state = 0;
           if (nz) {
             if (scale < 0.0) {
@@ -747,7 +760,11 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
         }
         if (first_state == 1) {
           acc_w = 0;
+          fast_ok = true;
         } else {
+          if constexpr (NW > 1) {
+            if (first_state >= 0) team_sync<NW>(team);  // s_rbv is rewritten below
+          }
           // qualification: G threads per column; state 0 no, 1 yes, 2 ambiguous
           {
             const int w = t / G, g = t % G;
@@ -827,29 +844,33 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
 
       // pivot row: argmax |u_hat| over unused rows, first index wins (aca.cpp:367, 375-376);
       // the column qualified, so the maximum is > 0 and zero rows never matter
-      double bv = 0.0;
-      int bi = 0x7fffffff;
+      double bv = fbv;
+      int bi = fbi;
+      if (!fast_ok) {
+        bv = 0.0;
+        bi = 0x7fffffff;
 #pragma unroll
-      for (int q = 0; q < RPL; ++q) {
-        const int i = t + q * TT;
-        if (rv[q] && !s_used[i]) {
-          const double av = fabs(acol[i]);
-          if (av > bv) {
-            bv = av;
-            bi = i;
+        for (int q = 0; q < RPL; ++q) {
+          const int i = t + q * TT;
+          if (rv[q] && !s_used[i]) {
+            const double av = fabs(acol[i]);
+            if (av > bv) {
+              bv = av;
+              bi = i;
+            }
           }
         }
-      }
-      warp_argmax_nonneg(bv, bi);
-      if constexpr (NW > 1) {
-        if (lane == 0) {
-          s_rbv[wib] = bv;
-          s_rbi[wib] = bi;
+        warp_argmax_nonneg(bv, bi);
+        if constexpr (NW > 1) {
+          if (lane == 0) {
+            s_rbv[wib] = bv;
+            s_rbi[wib] = bi;
+          }
+          team_sync<NW>(team);
+          bv = s_rbv[0];
+          bi = s_rbi[0];
+          for (int g = 1; g < NW; ++g) argmax_combine(bv, bi, s_rbv[g], s_rbi[g]);
         }
-        team_sync<NW>(team);
-        bv = s_rbv[0];
-        bi = s_rbi[0];
-        for (int g = 1; g < NW; ++g) argmax_combine(bv, bi, s_rbv[g], s_rbi[g]);
       }
       const int p = bi;
       if (r == 0 && t == 0) {  // scale2 = exact left fold of the first accepted column (aca.cpp:491)
