@@ -2140,6 +2140,15 @@ void launch_cluster(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, c
   HM_LAUNCH_CHECK();
 }
 
+// Split cluster barrier: arrive (release) ... independent work ... wait (acquire); together
+// exactly cluster.sync().
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acquire() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // ---------------------------------------------------------------------------
 // Smooth-path cluster kernel (1024 < max(m, n) <= 512 CL, k = 16): the smooth_kernel
 // schedule over a thread-block cluster of CL CTAs, with ONE cluster barrier per rank.
@@ -2210,17 +2219,22 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
     const double gm = static_cast<double>(m) * 1.2e-16;
     int k_eff = 0;
     bool fallback = false;
+    // raw candidate column entries A(i, r) of the own rows, one rank ahead: column r + 1 is
+    // evaluated between the arrive and the wait of rank r's cluster barrier (independent
+    // work hiding the barrier); column 0 here
+    double na0, na1;
+    {
+      double pc[DIM];
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) pc[a] = s_cc[a];
+      E.phi2(E.r2_pts(y0, pc), E.r2_pts(y1, pc), na0, na1);
+    }
+    const int rlast = min(kmax, n);
     for (int r = 0; r < kmax; ++r) {
       if (r >= n) break;
       const int par = r & 1;
       // column r residual of the own rows (candidate column r: no rejection so far)
-      double a0, a1;
-      {
-        double pc[DIM];
-#pragma unroll
-        for (int a = 0; a < DIM; ++a) pc[a] = s_cc[r * 4 + a];
-        E.phi2(E.r2_pts(y0, pc), E.r2_pts(y1, pc), a0, a1);
-      }
+      double a0 = na0, a1 = na1;
       SmoothChain<KC>::col2s<NCAP, KC>(a0, a1, s_u + t, s_u + t + TT, r, s_vc + r);
       // publish the residuals (the pivot value is read from its owner after the barrier)
       s_res[par * NCAP + t] = a0;
@@ -2262,7 +2276,15 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
         s_part[4 * par + 2] = cb;
         s_part[4 * par + 3] = static_cast<double>(ci);
       }
-      cluster.sync();  // the ONE barrier of the rank: partials and residuals published
+      // the ONE barrier of the rank: partials and residuals published
+      cluster_arrive_release();
+      if (r + 1 < rlast) {
+        double pc[DIM];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) pc[a] = s_cc[(r + 1) * 4 + a];
+        E.phi2(E.r2_pts(y0, pc), E.r2_pts(y1, pc), na0, na1);
+      }
+      cluster_wait_acquire();
       // identical decision in every CTA: partials combined in rank order
       {
         double ps[CL][4];
