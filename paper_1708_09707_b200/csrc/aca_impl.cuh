@@ -202,6 +202,24 @@ struct KernelEntry {
       c1 = eval(z1, jc);
     }
   }
+  // row y against four points (bitwise four eval() calls)
+  __device__ __forceinline__ void eval4c(const double* y, long long j0, long long j1, long long j2, long long j3,
+                                         double& a0, double& a1, double& a2, double& a3) const {
+    if constexpr (KIND >= 0) {
+      const double r2[4] = {r2_of(y, j0), r2_of(y, j1), r2_of(y, j2), r2_of(y, j3)};
+      double f[4];
+      phi_xv<KIND, 4>(kp, r2, f);
+      a0 = f[0];
+      a1 = f[1];
+      a2 = f[2];
+      a3 = f[3];
+    } else {
+      a0 = eval(y, j0);
+      a1 = eval(y, j1);
+      a2 = eval(y, j2);
+      a3 = eval(y, j3);
+    }
+  }
   __device__ __forceinline__ void eval2c(const double* y, long long j0, long long j1, double& a0, double& a1) const {
     if constexpr (KIND >= 0) {
       phi_x2<KIND>(kp, r2_of(y, j0), r2_of(y, j1), a0, a1);
@@ -1641,7 +1659,28 @@ __global__ void __launch_bounds__(kBigThreads, 2) aca_big_kernel(AcaJob J, Kerne
         double uP[KC];  // u_l[p], right-aligned: every V-row load of the chain issues up front
 #pragma unroll
         for (int j = 0; j < KC; ++j) uP[j] = j >= KC - r ? s_up[j - (KC - r)] : 0.0;
-        for (int j = t; j < n; j += 2 * TT) {
+        // no window columns (the one-column path): four columns per step, one 4-way
+        // evaluation (independent K1 / exp chains) and two chains
+        const int jstart = (KC == 16 && filled == 0) ? n : t;
+        if constexpr (KC == 16) {
+          for (int j = t; filled == 0 && j < n; j += 4 * TT) {
+            long long jq[4];
+            bool okq[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              okq[q] = j + q * TT < n;
+              jq[q] = okq[q] ? j + q * TT : j;
+            }
+            double a[4];
+            E.eval4c(yp, cl + jq[0], cl + jq[1], cl + jq[2], cl + jq[3], a[0], a[1], a[2], a[3]);
+            SmoothChain<16>::row2<1>(a[0], a[1], s_up, V + jq[0] * kmax, V + jq[1] * kmax, r);
+            SmoothChain<16>::row2<1>(a[2], a[3], s_up, V + jq[2] * kmax, V + jq[3] * kmax, r);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (okq[q]) V[jq[q] * kmax + r] = a[q];
+          }
+        }
+        for (int j = jstart; j < n; j += 2 * TT) {
           const int j1 = j + TT;
           const bool ok1 = j1 < n;
           const int jj = ok1 ? j1 : j;

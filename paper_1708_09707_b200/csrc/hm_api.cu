@@ -963,7 +963,7 @@ hm_status hm_get_stats(hm_handle* H, hm_stats* st) {
     st->dmax_leaf = h.dmax_leaf;
     st->row_begin = h.row_begin;
     st->row_end = h.row_end;
-    st->device_bytes = static_cast<double>(h.dense_vals.bytes() + h.U.bytes() + h.V.bytes() + h.coords.bytes());
+    st->device_bytes = static_cast<double>(h.dense_vals.bytes() + h.U.bytes() + h.V.bytes() + h.U2.bytes() + h.V2.bytes() + h.coords.bytes());
     st->S_d_stored = h.S_d_stored;
     st->near_sym = h.near_sym ? 1 : 0;
     st->n_aca_batches = h.n_batches;

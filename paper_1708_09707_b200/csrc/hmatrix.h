@@ -84,6 +84,7 @@ struct HandleStreams {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_last = nullptr;  // end of the last work on `stream` (orders caller streams)
   cudaEvent_t ev_ph[4] = {};      // MvpTimings: near [0,1), far [2,3)
+  cudaEvent_t ev_chunk[5] = {};   // recompute overlap: [b] factors of buffer b ready, [2+b] applied, [4] join
   void create(int dev);           // streams + events (throws HM_ECUDA)
   ~HandleStreams();
 };
@@ -122,6 +123,10 @@ struct HMatrix : HandleStreams {
   // admissible-block factors: U rank-major (kmax x m), V interleaved (n x kmax)
   DevBuf<long long> u_off, v_off;  // per aca leaf (also per-chunk in recompute mode)
   DevBuf<double> U, V;
+  // recompute mode: a second factor workspace, so chunk c+1 is factorised (stream) while
+  // chunk c's far field is applied (aux stream) -- each workspace half the chunk budget
+  DevBuf<double> U2, V2;
+  bool chunk_overlap = false;
   // Regular geometry (N = S * 2^dmax_leaf, S a power of two <= 256, k even) with stored
   // factors: U is row-tiled by S rows ([i/S][l][i%S]) and the product runs the
   // TMA-pipelined cluster kernel; otherwise U is rank-major (kmax x m).

@@ -1522,8 +1522,16 @@ void plan_far_field(HMatrix& h, cudaStream_t s) {
   if (!h.cfg.precompute_aca) {
     size_t free_b = 0, total_b = 0;
     HM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    // HM_OVERLAP=1: two workspaces of half the budget, chunk c+1's factorisation (FP64-bound)
+    // beside chunk c's far-field apply (HBM-bound) on the auxiliary stream.  Measured slower
+    // (config 3: 4.92 vs 4.53 s; config-5 geometry 10.07 vs 9.84 s): twice the chunks, twice
+    // the class-kernel tails, and the apply competes with the factorisation for the SMs.
+    // Default: one workspace, chunks factorised and applied in turn.
+    const char* eo = std::getenv("HM_OVERLAP");
+    h.chunk_overlap = h.aux != nullptr && (eo ? std::atoi(eo) != 0 : false);
     budget = h.cfg.aca_chunk_rows > 0 ? h.cfg.aca_chunk_rows * kmax * 16
-                                      : std::min<long long>(static_cast<long long>(free_b / 2), 96ll << 30);
+                                      : std::min<long long>(static_cast<long long>(free_b / 2), 96ll << 30) /
+                                            (h.chunk_overlap ? 2 : 1);
     budget = std::max(budget, 1ll << 20);
   }
   h.chunks.clear();
@@ -1716,7 +1724,22 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
   const long long kmax = h.cfg.k;
   const bool trace = std::getenv("HM_TRACE") != nullptr;
   reset_aca_rejections(h, s);
-  for (const AcaChunk& c : h.chunks) {
+  // two factor workspaces (U, V) and (U2, V2) alternate by chunk parity: chunk c's apply
+  // runs on the auxiliary stream once its factors are ready, and chunk c+2's factorisation
+  // waits until that apply has read them (serial while tracing or timing kernels)
+  const bool ovl = h.chunk_overlap && h.chunks.size() > 1 && !trace && !h.clk.on;
+  if (ovl) {
+    HM_CUDA(cudaEventRecord(h.ev_fork, s));  // after the near field (z partial sums)
+    HM_CUDA(cudaStreamWaitEvent(h.aux, h.ev_fork, 0));
+  }
+  for (size_t ci = 0; ci < h.chunks.size(); ++ci) {
+    const AcaChunk& c = h.chunks[ci];
+    const int buf = ovl ? static_cast<int>(ci & 1) : 0;
+    if (buf) {  // every launch below reads h.U / h.V at launch time
+      std::swap(h.U, h.U2);
+      std::swap(h.V, h.V2);
+    }
+    if (ovl && ci >= 2) HM_CUDA(cudaStreamWaitEvent(s, h.ev_chunk[2 + buf], 0));
     const auto tc0 = std::chrono::steady_clock::now();
     // the workspace is allocated by the first product and reused
     if (h.U.size() < static_cast<size_t>(c.ue - c.ub)) h.U.alloc(c.ue - c.ub, s);
@@ -1725,6 +1748,12 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
     h.clk.start(kKAca, s);
     compute_aca(h, c, s);
     h.clk.stop(kKAca, s);
+    cudaStream_t sa = s;
+    if (ovl) {
+      HM_CUDA(cudaEventRecord(h.ev_chunk[buf], s));
+      HM_CUDA(cudaStreamWaitEvent(h.aux, h.ev_chunk[buf], 0));
+      sa = h.aux;
+    }
     if (trace) {
       HM_CUDA(cudaStreamSynchronize(s));
       const auto tc2 = std::chrono::steady_clock::now();
@@ -1732,9 +1761,9 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
                    8.0 * (c.ue - c.ub + c.ve - c.vb) / 1e9, std::chrono::duration<double, std::milli>(tc1 - tc0).count(),
                    std::chrono::duration<double, std::milli>(tc2 - tc1).count());
     }
-    h.clk.start(kKLowrankT, s);
-    launch_t(h, h.sched_order.get() + c.sched_off, c.c1 - c.c0, c.vb, s);
-    h.clk.stop(kKLowrankT, s);
+    h.clk.start(kKLowrankT, sa);
+    launch_t(h, h.sched_order.get() + c.sched_off, c.c1 - c.c0, c.vb, sa);
+    h.clk.stop(kKLowrankT, sa);
     RowArgs b = base_row_args(h);
     b.z_in = h.zm.get();
     b.a_ubase = c.ub;
@@ -1743,7 +1772,7 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
     // only the rows the chunk's leaves touch (the others keep their partial sums)
     b.row_begin = std::max<long long>(h.row_begin, c.row_lo);
     b.row_end = std::min<long long>(h.row_end, c.row_hi);
-    h.clk.start(kKRowsFar, s);
+    h.clk.start(kKRowsFar, sa);
     if (h.tma_far) {
       const long long S = h.n >> h.dmax_leaf;
       b.row_begin = b.row_begin / S * S;
@@ -1756,16 +1785,25 @@ void mvp_morton(HMatrix& h, cudaStream_t s) {
       A.far_only = 1;
       const unsigned ncl = static_cast<unsigned>((b.row_end - b.row_begin) / S);
       if (ncl > 0) {
-        if (S == 64 && kmax <= 16) rows_tma_kernel<64, 16, 5><<<ncl, 64, 0, s>>>(A);
-        else if (S == 64) rows_tma_kernel<64, 32, 2><<<ncl, 64, 0, s>>>(A);
-        else if (kmax <= 16) rows_tma_kernel<32, 16, 8><<<ncl, 32, 0, s>>>(A);
-        else rows_tma_kernel<32, 32, 5><<<ncl, 32, 0, s>>>(A);
+        if (S == 64 && kmax <= 16) rows_tma_kernel<64, 16, 5><<<ncl, 64, 0, sa>>>(A);
+        else if (S == 64) rows_tma_kernel<64, 32, 2><<<ncl, 64, 0, sa>>>(A);
+        else if (kmax <= 16) rows_tma_kernel<32, 16, 8><<<ncl, 32, 0, sa>>>(A);
+        else rows_tma_kernel<32, 32, 5><<<ncl, 32, 0, sa>>>(A);
         HM_LAUNCH_CHECK();
       }
     } else {
-      dispatch_rows(h, b, 0, true, s);
+      dispatch_rows(h, b, 0, true, sa);
     }
-    h.clk.stop(kKRowsFar, s);
+    h.clk.stop(kKRowsFar, sa);
+    if (ovl) HM_CUDA(cudaEventRecord(h.ev_chunk[2 + buf], h.aux));
+    if (buf) {
+      std::swap(h.U, h.U2);
+      std::swap(h.V, h.V2);
+    }
+  }
+  if (ovl) {
+    HM_CUDA(cudaEventRecord(h.ev_chunk[4], h.aux));
+    HM_CUDA(cudaStreamWaitEvent(s, h.ev_chunk[4], 0));
   }
   h.keff_known = true;
   phase_mark(h, 3, s);

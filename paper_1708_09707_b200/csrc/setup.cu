@@ -513,6 +513,7 @@ void HandleStreams::create(int dev) {
   HM_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
   HM_CUDA(cudaEventCreateWithFlags(&ev_last, cudaEventDisableTiming));
   for (cudaEvent_t& e : ev_ph) HM_CUDA(cudaEventCreate(&e));
+  for (cudaEvent_t& e : ev_chunk) HM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 }
 
 HandleStreams::~HandleStreams() {
@@ -522,6 +523,8 @@ HandleStreams::~HandleStreams() {
   if (stream) cudaStreamDestroy(stream);
   if (aux) cudaStreamDestroy(aux);
   for (cudaEvent_t e : {ev_fork, ev_join, ev_last, ev_ph[0], ev_ph[1], ev_ph[2], ev_ph[3]})
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : ev_chunk)
     if (e) cudaEventDestroy(e);
 }
 

@@ -262,3 +262,36 @@ def test_batch_sweep_csv(gpu):
     assert [int(r[0]) for r in rows[6:]] == [0] + [1 << e for e in range(16, 25, 2)]
     assert all(r[2:6] == ["2048", "2", "16", "64"] for r in rows)
     assert all(float(r[6]) > 0 and float(r[7]) > 0 for r in rows)
+
+
+@pytest.mark.parametrize("kern,d", [("gaussian", 2), ("matern", 3)])
+def test_recompute_chunk_overlap_bitwise_and_capturable(gpu, monkeypatch, kern, d):
+    """Recompute mode with several chunks: two factor workspaces, chunk c+1 factorised
+    while chunk c's far field is applied on the auxiliary stream (HM_OVERLAP=1, opt-in)
+    gives the bits of the serial schedule, and the forked product still captures into a
+    CUDA graph whose replays are bitwise equal."""
+    import torch
+    n = 1 << 14
+    P = uniform_points(n, d, 42)
+    x = symmetric(5, n)
+    out = {}
+    for ov in ("0", "1"):
+        monkeypatch.setenv("HM_OVERLAP", ov)
+        h = gpu.setup(P, gpu.KernelFunction(kern), gpu.HmatrixConfig(c_leaf=64, k=16, aca_chunk_rows=64,
+                                                                             bs_aca=1 << 12))
+        assert h.stats()["n_aca_chunks"] >= 2
+        out[ov] = (h, h.mvp(x))
+    assert np.array_equal(bits(out["0"][1]), bits(out["1"][1]))
+    h = out["1"][0]
+    xd = torch.from_numpy(x).cuda()
+    z = torch.empty(n, dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        h.mvp_device(xd.data_ptr(), z.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    for t in range(2):
+        xh = symmetric(200 + t, n)
+        xd.copy_(torch.from_numpy(xh))
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(z.cpu().numpy()), bits(out["0"][0].mvp(xh))), t
