@@ -1053,6 +1053,58 @@ void launch_win(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, cudaS
 // there from scratch, so every block's factors are bitwise the reference's either way.
 // PRE: the k raw candidate columns are evaluated up front into shared memory (more
 // shared memory per team, fewer teams per SM) or each rank's column is evaluated in place.
+// Compact residual chains of the smooth kernels (HM_SMOOTH_ROLLED): the same
+// left folds as SmoothChain (l = 0 .. r-1 in order: bitwise identical), as a loop of four
+// predicated steps whose loads issue together, instead of a straight-line case per r --
+// O(k) instead of O(k^2) code in the kernels' hot loop (instruction-cache misses were
+// 16-21% of the smooth kernels' stall samples).  Indices past r are clamped to k - 1
+// (valid shared-memory addresses, results unused).
+#ifndef HM_SMOOTH_ROLLED
+#define HM_SMOOTH_ROLLED 1
+#endif
+template <int KC, int US, int VS>
+__device__ __forceinline__ void col2_rolled(double& a0, double& a1, const double* u0, const double* u1, int r,
+                                            const double* vb) {
+#pragma unroll 1
+  for (int l0 = 0; l0 < r; l0 += 4) {
+    double x0[4], x1[4], w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int l = min(l0 + q, KC - 1);
+      x0[q] = u0[l * US];
+      x1[q] = u1[l * US];
+      w[q] = vb[l * VS];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (l0 + q < r) {
+        a0 = hsub(a0, hmul(x0[q], w[q]));
+        a1 = hsub(a1, hmul(x1[q], w[q]));
+      }
+  }
+}
+template <int KC, int VS, int US>
+__device__ __forceinline__ void row2_rolled(double& b0, double& b1, const double* up, const double* vb0,
+                                            const double* vb1, int r) {
+#pragma unroll 1
+  for (int l0 = 0; l0 < r; l0 += 4) {
+    double w[4], x0[4], x1[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int l = min(l0 + q, KC - 1);
+      w[q] = up[l * US];
+      x0[q] = vb0[l * VS];
+      x1[q] = vb1[l * VS];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (l0 + q < r) {
+        b0 = hsub(b0, hmul(w[q], x0[q]));
+        b1 = hsub(b1, hmul(w[q], x1[q]));
+      }
+  }
+}
+
 template <int NW, bool PRE>
 __host__ __device__ constexpr size_t smooth_stride() {
   return (PRE ? static_cast<size_t>(16) * (NW * 64 + 1) : static_cast<size_t>(NW * 64 + 1) + 64) +
@@ -1063,6 +1115,9 @@ template <int DIM, int KIND, int NW, bool PRE>
 __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntry<DIM, KIND> E, int teams_per_cta) {
   constexpr int KC = 16;
   constexpr int TT = NW * 32, NCAP = 2 * TT, CS = NCAP + 1;
+  // compact chains where measured faster (config 3 / config-5 geometry, per class): NW = 1
+  // -10% / -11%, NW = 2 Matern -5% (Gaussian +2%), NW = 4 +3% / +8% (straight-line kept)
+  constexpr bool kRolled = HM_SMOOTH_ROLLED && (NW == 1 || (NW == 2 && KIND == 1));
   static_assert(DIM > 0, "smooth kernel: compile-time dimension");
   extern __shared__ double smem[];
   const int team = threadIdx.x / TT, t = threadIdx.x % TT, lane = t & 31, wib = t >> 5;
@@ -1139,7 +1194,8 @@ __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntr
         E.phi2(E.r2_pts(y0, pc), E.r2_pts(y1, pc), a0, a1);
         if (!rv1) a1 = 0.0;
       }
-      SmoothChain<KC>::col2s<NCAP>(a0, a1, s_u + t, s_u + t + TT, r, s_v + r);
+      if constexpr (kRolled) col2_rolled<KC, NCAP, NCAP>(a0, a1, s_u + t, s_u + t + TT, r, s_v + r);
+      else SmoothChain<KC>::col2s<NCAP>(a0, a1, s_u + t, s_u + t + TT, r, s_v + r);
       // fused reduction: norm2 (any order, bounded), argmax over unused rows; the nonzero
       // flag is "maximum > 0" (|u_hat| >= 0, no candidate = +0)
       double sum = 0.0, bv = 0.0;
@@ -1259,7 +1315,8 @@ __global__ void __launch_bounds__(128, 3) aca_smooth_kernel(AcaJob J, KernelEntr
         const bool cv0 = j0 < n, cv1 = j1 < n;
         double b0, b1;
         E.phi2(E.r2_pts(yp, yc0), E.r2_pts(yp, yc1), b0, b1);
-        SmoothChain<KC>::row2<NCAP, NCAP>(b0, b1, s_u + p, s_v + j0, s_v + j1, r);
+        if constexpr (kRolled) row2_rolled<KC, NCAP, NCAP>(b0, b1, s_u + p, s_v + j0, s_v + j1, r);
+        else SmoothChain<KC>::row2<NCAP, NCAP>(b0, b1, s_u + p, s_v + j0, s_v + j1, r);
         if (cv0) s_v[r * NCAP + j0] = b0;
         if (cv1) s_v[r * NCAP + j1] = b1;
       }
