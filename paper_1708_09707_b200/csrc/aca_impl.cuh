@@ -2354,23 +2354,23 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
       int nz = bv > 0.0 ? 1 : 0;
       if (lane == 0) {
         s_red[4 * wib] = sum;
-        s_red[4 * wib + 1] = static_cast<double>(nz);
         s_red[4 * wib + 2] = bv;
         s_red[4 * wib + 3] = static_cast<double>(bi);
       }
       __syncthreads();
-      if (t == 0) {
-        double cs = s_red[0], cb = s_red[2];
-        int cn = static_cast<int>(s_red[1]), ci = static_cast<int>(s_red[3]);
-        for (int w = 1; w < TT / 32; ++w) {
-          cs = hadd(cs, s_red[4 * w]);
-          cn |= static_cast<int>(s_red[4 * w + 1]);
-          argmax_combine(cb, ci, s_red[4 * w + 2], static_cast<int>(s_red[4 * w + 3]));
+      // CTA partial: warp 0 combines the 8 warps' partials with one butterfly (the norm2's
+      // summation order is free -- rigorous bound; argmax and the flag are order-free)
+      if (wib == 0) {
+        double cs = lane < TT / 32 ? s_red[4 * lane] : 0.0, cb = lane < TT / 32 ? s_red[4 * lane + 2] : 0.0;
+        int ci = lane < TT / 32 ? static_cast<int>(s_red[4 * lane + 3]) : 0x7fffffff;
+#pragma unroll
+        for (int o = TT / 64; o; o >>= 1) cs = hadd(cs, __shfl_xor_sync(0xffffffffu, cs, o));
+        warp_argmax_nonneg(cb, ci);
+        if (lane == 0) {
+          s_part[4 * par] = cs;
+          s_part[4 * par + 2] = cb;
+          s_part[4 * par + 3] = static_cast<double>(ci);
         }
-        s_part[4 * par] = cs;
-        s_part[4 * par + 1] = static_cast<double>(cn);
-        s_part[4 * par + 2] = cb;
-        s_part[4 * par + 3] = static_cast<double>(ci);
       }
       // the ONE barrier of the rank: partials and residuals published
       cluster_arrive_release();
@@ -2381,25 +2381,26 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
         E.phi2(E.r2_pts(y0, pc), E.r2_pts(y1, pc), na0, na1);
       }
       cluster_wait_acquire();
-      // identical decision in every CTA: partials combined in rank order
+      // identical decision in every CTA and warp: lane c < CL reads CTA c's partial (CL
+      // remote loads per warp instead of CL x 4 per thread), one fixed butterfly combines
+      // them (commutative at every node: the same bits in every lane, warp and CTA); the
+      // nonzero flag is "maximum > 0" as in the smooth kernel
       {
-        double ps[CL][4];
-#pragma unroll
-        for (int c = 0; c < CL; ++c) {
-          const double* q = rem(s_part + 4 * par, c);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) ps[c][e] = q[e];
+        double ps = 0.0, pb = 0.0;
+        int pi = 0x7fffffff;
+        if (lane < CL) {
+          const double* q = rem(s_part + 4 * par, lane);
+          ps = q[0];
+          pb = q[2];
+          pi = static_cast<int>(q[3]);
         }
-        sum = ps[0][0];
-        nz = static_cast<int>(ps[0][1]);
-        bv = ps[0][2];
-        bi = static_cast<int>(ps[0][3]);
 #pragma unroll
-        for (int c = 1; c < CL; ++c) {
-          sum = hadd(sum, ps[c][0]);
-          nz |= static_cast<int>(ps[c][1]);
-          argmax_combine(bv, bi, ps[c][2], static_cast<int>(ps[c][3]));
-        }
+        for (int o = CL / 2; o; o >>= 1) ps = hadd(ps, __shfl_xor_sync(0xffffffffu, ps, o));
+        warp_argmax_nonneg(pb, pi);
+        sum = ps;
+        bv = pb;
+        bi = pi;
+        nz = bv > 0.0 ? 1 : 0;
       }
       int st = 0;
       if (nz) {
