@@ -204,6 +204,11 @@ void compute_aca(HMatrix& h, const AcaChunk& c, cudaStream_t s) {
   J.rejections = h.aca_rej.get();
   J.evals = nullptr;
   J.tile_shift = h.u_tile_shift;
+  {
+    // window kernels: one fresh column per rank until a rejection, d >= 3 (HM_WIN_ONE=0/1)
+    const char* ew = std::getenv("HM_WIN_ONE");
+    J.win_one = (ew ? std::atoi(ew) != 0 : h.d >= 3) ? 1 : 0;
+  }
   const int* jobs = h.sched_jobs.get() + c.sched_off;
   const long long* ccount = c.ccount;
   int sms = 0;

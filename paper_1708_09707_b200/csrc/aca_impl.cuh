@@ -256,6 +256,7 @@ struct AcaJob {
   const int* njobs_dev = nullptr;  // job count on the device (fallback lists), overrides njobs
   int* fb_list = nullptr;   // smooth kernel: blocks that hit a rejection are appended here
   int* fb_count = nullptr;
+  int win_one = 0;          // window kernels: one fresh column per rank until a rejection (d >= 3)
   // explicit-matrix seam: block b entries at dense + dense_off[b], row-major m x n
   const double* dense;
   const long long* dense_off;
@@ -695,7 +696,8 @@ __global__ void __launch_bounds__(NW * 32 < 128 ? 128 : NW * 32, MINB)
       while (next < n) {
         // speculation depth: while no column was rejected, at most kmax - r more can be
         // accepted (smooth blocks, d >= 3: no noise floor), so do not evaluate past them
-        const int lim = rejections ? W : max(kmax - r, 1);
+        // (win_one, d >= 3: one fresh column per rank, no speculative columns to cross-update)
+        const int lim = rejections ? W : (J.win_one ? 1 : max(kmax - r, 1));
         const int wcols = max(filled, min(min(W, lim), n - next));
         ev_col += static_cast<unsigned long long>(wcols - filled) * m;
         // fill: fresh window columns, entry then the reference chain over l < r
@@ -2397,7 +2399,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
 #pragma unroll
         for (int o = CL / 2; o; o >>= 1) ps = hadd(ps, __shfl_xor_sync(0xffffffffu, ps, o));
         warp_argmax_nonneg(pb, pi);
-        sum = ps;
+        sum = __shfl_sync(0xffffffffu, ps, 0);  // lanes >= CL folded zeros: lane 0's value for all
         bv = pb;
         bi = pi;
         nz = bv > 0.0 ? 1 : 0;
