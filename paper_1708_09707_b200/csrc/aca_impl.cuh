@@ -2272,9 +2272,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
   double* s_u = smem;                     // KC x NCAP: u_l of the own rows
   double* s_res = s_u + KC * NCAP;        // 2 x NCAP: residuals of the own rows (rank parity)
   double* s_vc = s_res + 2 * NCAP;        // KC x KC: v_l at the candidate columns
-  double* s_part = s_vc + KC * KC;        // 2 x 4: CTA partial (rank parity)
-  double* s_red = s_part + 8;             // 8 warps x 4
-  double* s_up = s_red + 32;              // KC: u_l[p]
+  double* s_part = s_vc + KC * KC;        // 2 x 8: CTA partial + its argmax row's point (rank parity)
+  double* s_red = s_part + 16;            // 8 warps x 8: warp partial + its argmax row's point
+  double* s_up = s_red + 64;              // KC: u_l[p]
   double* s_misc = s_up + KC;             // [0] job [1] pivot value
   double* s_cc = s_misc + 8;              // KC x 4: points of the candidate columns
   const int t = threadIdx.x, lane = t & 31, wib = t >> 5;
@@ -2355,23 +2355,33 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
       warp_argmax_nonneg(bv, bi);
       int nz = bv > 0.0 ? 1 : 0;
       if (lane == 0) {
-        s_red[4 * wib] = sum;
-        s_red[4 * wib + 2] = bv;
-        s_red[4 * wib + 3] = static_cast<double>(bi);
+        s_red[8 * wib] = sum;
+        s_red[8 * wib + 2] = bv;
+        s_red[8 * wib + 3] = static_cast<double>(bi);
+      }
+      // the warp winner's point, from its owner's registers (published with the partial, so
+      // the pivot point needs no dependent global load after the cluster barrier)
+      if (bi == i0 || bi == i1) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) s_red[8 * wib + 4 + a] = bi == i0 ? y0[a] : y1[a];
       }
       __syncthreads();
       // CTA partial: warp 0 combines the 8 warps' partials with one butterfly (the norm2's
       // summation order is free -- rigorous bound; argmax and the flag are order-free)
       if (wib == 0) {
-        double cs = lane < TT / 32 ? s_red[4 * lane] : 0.0, cb = lane < TT / 32 ? s_red[4 * lane + 2] : 0.0;
-        int ci = lane < TT / 32 ? static_cast<int>(s_red[4 * lane + 3]) : 0x7fffffff;
+        double cs = lane < TT / 32 ? s_red[8 * lane] : 0.0, cb = lane < TT / 32 ? s_red[8 * lane + 2] : 0.0;
+        int ci = lane < TT / 32 ? static_cast<int>(s_red[8 * lane + 3]) : 0x7fffffff;
 #pragma unroll
         for (int o = TT / 64; o; o >>= 1) cs = hadd(cs, __shfl_xor_sync(0xffffffffu, cs, o));
         warp_argmax_nonneg(cb, ci);
         if (lane == 0) {
-          s_part[4 * par] = cs;
-          s_part[4 * par + 2] = cb;
-          s_part[4 * par + 3] = static_cast<double>(ci);
+          s_part[8 * par] = cs;
+          s_part[8 * par + 2] = cb;
+          s_part[8 * par + 3] = static_cast<double>(ci);
+        }
+        if (ci != 0x7fffffff && lane < DIM) {
+          const int w = ((ci - row0) % TT) >> 5;  // the warp owning row ci
+          s_part[8 * par + 4 + lane] = s_red[8 * w + 4 + lane];
         }
       }
       // the ONE barrier of the rank: partials and residuals published
@@ -2391,7 +2401,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
         double ps = 0.0, pb = 0.0;
         int pi = 0x7fffffff;
         if (lane < CL) {
-          const double* q = rem(s_part + 4 * par, lane);
+          const double* q = rem(s_part + 8 * par, lane);
           ps = q[0];
           pb = q[2];
           pi = static_cast<int>(q[3]);
@@ -2426,7 +2436,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
       // u_l[p] (l < r) and the pivot value from the owner CTA
       if (t < r) s_up[t] = *rem(s_u + t * NCAP + pl, po);
       if (t == KC) s_misc[1] = *rem(s_res + par * NCAP + pl, po);
-      if (t >= 32 && t < 32 + DIM) s_misc[2 + t - 32] = __ldg(E.coords + (t - 32) * E.n + rl + p);  // pivot point
+      if (t >= 32 && t < 32 + DIM) s_misc[2 + t - 32] = *rem(s_part + 8 * par + 4 + (t - 32), po);  // pivot point
       if (po == cr && t == (pl % TT)) {
         if (pl >= TT) used1 = true;
         else used0 = true;
@@ -2519,7 +2529,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
 template <int DIM, int KIND, int CL>
 void launch_smooth_cluster(const AcaJob& J, const KernelEntry<DIM, KIND>& E, int sms, cudaStream_t s) {
   if (J.njobs <= 0) return;
-  const size_t smem = sizeof(double) * (16 * 512 + 2 * 512 + 16 * 16 + 8 + 32 + 16 + 8 + 64);
+  const size_t smem = sizeof(double) * (16 * 512 + 2 * 512 + 16 * 16 + 16 + 64 + 16 + 8 + 64);
   auto kfn = aca_smooth_cluster_kernel<DIM, KIND, CL>;
   HM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const long long clusters = std::min<long long>(J.njobs, std::max(1, 2 * sms / CL));
